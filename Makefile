@@ -1,0 +1,33 @@
+# Build for B200 (sm_100a) only. Product: paper_1109_3524_b200/libibmgpu.so (C-ABI, include/ibmgpu.h).
+# Test infrastructure (CPU checkers): oracle/liboracle.so, oracle/_ref/libibmref.so (see oracle/Makefile).
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+PKG := paper_1109_3524_b200
+SRC := $(wildcard $(PKG)/csrc/*.cu)
+HOST := $(wildcard $(PKG)/csrc/host/*.cpp)
+HDR := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/host/*.hpp) include/ibmgpu.h
+OBJDIR := build/obj
+OBJ := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(SRC)) $(patsubst $(PKG)/csrc/host/%.cpp,$(OBJDIR)/host_%.o,$(HOST))
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp -Xptxas -v --expt-relaxed-constexpr
+HOSTFLAGS := -O3 -std=c++17 -fPIC -fopenmp -ffp-contract=off
+
+all: $(PKG)/libibmgpu.so oracle
+
+$(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
+
+$(OBJDIR)/host_%.o: $(PKG)/csrc/host/%.cpp $(HDR)
+	@mkdir -p $(OBJDIR)
+	g++ $(HOSTFLAGS) -I/usr/local/cuda/include -c $< -o $@
+
+$(PKG)/libibmgpu.so: $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -Xcompiler -fopenmp -lcudart_static -lrt -ldl -lpthread
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf build $(PKG)/libibmgpu.so
+
+.PHONY: all oracle clean

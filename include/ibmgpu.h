@@ -1,0 +1,222 @@
+/* ibmgpu.h — C-ABI of the B200-native IBPM sparse linear-algebra hot path.
+ *
+ * Drop-in boundary for the reference's in-process operator API
+ * (/root/reference/proj/include/ibm/*.hpp; the reference is header-only C++ with no FFI,
+ * so each entry point below names the C++ function/method it replaces). Plain pointers
+ * and sizes only; no torch or CUDA types in any signature. `*_dev` arguments are device
+ * pointers obtained from ibmgpu_vec_alloc (or any cudaMalloc'd memory on the context's
+ * device); everything else is host memory.
+ *
+ * Error convention: every function returns 0 on success or an IBMGPU_E* code;
+ * the message is in ibmgpu_last_error(ctx). Codes map 1:1 onto the reference's exceptions:
+ *   IBMGPU_EINVAL   -> std::invalid_argument (sparse.hpp:39,114,227,286; krylov.hpp:22-23,55,74-82; amg.hpp:128,147)
+ *   IBMGPU_ESUPPORT -> std::runtime_error whose message contains "uniform" (operators.hpp:251-256)
+ *   IBMGPU_ECUDA / IBMGPU_ENCCL / IBMGPU_ENOMEM -> std::runtime_error
+ * Non-convergence and breakdown are NOT errors: they travel in ibm_solve_result.status, exactly
+ * as SolveStatus does (krylov.hpp:27).
+ *
+ * Threading: one host thread drives one context; calls are ordered on the context's stream and
+ * are not reentrant (as Stepper, stepper.hpp:167-168).
+ */
+#ifndef IBMGPU_H
+#define IBMGPU_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IBMGPU_OK 0
+#define IBMGPU_EINVAL 1
+#define IBMGPU_ESUPPORT 2
+#define IBMGPU_ECUDA 3
+#define IBMGPU_ENCCL 4
+#define IBMGPU_ENOMEM 5
+
+typedef struct ibmgpu_ctx* ibmgpu_ctx_t;
+typedef struct ibmgpu_mat* ibmgpu_mat_t;
+typedef struct ibmgpu_hier* ibmgpu_hier_t;
+typedef struct ibmgpu_stepper* ibmgpu_stepper_t;
+
+/* krylov.hpp:15-25 SolverParams */
+typedef struct {
+    double rel_tol;     /* default 1e-5 */
+    int max_iters;      /* default 2000 */
+    int record_history; /* history is copied to ibmgpu_pcg's history_host when non-zero */
+    int check_symmetry; /* max|A-A^T| <= 1e-12 max|A| checked on the device */
+} ibm_solver_params;
+
+/* krylov.hpp:27-37 SolveResult (x stays on the device) */
+typedef struct {
+    int iterations;
+    double rel_residual;
+    int status; /* 0 converged, 1 max_iterations, 2 breakdown (SolveStatus order) */
+    int history_len;
+} ibm_solve_result;
+
+/* amg.hpp:21-31 SaOptions */
+typedef struct {
+    double theta;
+    int max_coarse;
+    int max_levels;
+    int power_iterations;
+    int keep_fine_tail;
+} ibm_sa_options;
+
+/* Preconditioner kinds for ibmgpu_pcg (krylov.hpp:46-66, amg.hpp:237-246) */
+#define IBMGPU_PC_IDENTITY 0
+#define IBMGPU_PC_DIAGONAL 1
+#define IBMGPU_PC_SA 2
+
+/* ---------------------------------------------------------------- context / memory */
+/* One context per GPU: owns the stream, the memory pool, cached graphs and (rank>0 runs) the
+ * NCCL communicator. nranks=1, rank=0, nccl_id=NULL for single-GPU use. */
+int ibmgpu_init(int device, int nranks, int rank, const void* nccl_id, ibmgpu_ctx_t* ctx);
+int ibmgpu_destroy(ibmgpu_ctx_t ctx);
+const char* ibmgpu_last_error(ibmgpu_ctx_t ctx);
+const char* ibmgpu_version(void);
+int ibmgpu_synchronize(ibmgpu_ctx_t ctx);
+int ibmgpu_vec_alloc(ibmgpu_ctx_t ctx, size_t n_doubles, double** dev);
+int ibmgpu_vec_free(ibmgpu_ctx_t ctx, double* dev);
+int ibmgpu_h2d(ibmgpu_ctx_t ctx, double* dev, const double* host, size_t n);
+int ibmgpu_d2h(ibmgpu_ctx_t ctx, double* host, const double* dev, size_t n);
+/* device-side timing on the context stream: start, stop -> milliseconds */
+int ibmgpu_timer_start(ibmgpu_ctx_t ctx);
+int ibmgpu_timer_stop(ibmgpu_ctx_t ctx, float* ms);
+/* number of this library's kernels launched on the context since init (graph nodes included) */
+int ibmgpu_launch_count(ibmgpu_ctx_t ctx, long long* n);
+
+/* ---------------------------------------------------------------- CSR (sparse.hpp:27-222) */
+/* SparseMatrix(rows, cols, row_ptr, col_idx, values) (sparse.hpp:31-34): the CSR is taken as is
+ * (strictly increasing columns per row assumed, as the reference's invariant). */
+int ibmgpu_csr_upload(ibmgpu_ctx_t ctx, int rows, int cols, int nnz, const int* rptr, const int* cidx,
+                      const double* val, ibmgpu_mat_t* out);
+/* SparseMatrix::from_triplets (sparse.hpp:36-67): sort, sum duplicates, drop exact zeros */
+int ibmgpu_csr_from_triplets(ibmgpu_ctx_t ctx, int rows, int cols, int n, const int* r, const int* c,
+                             const double* v, ibmgpu_mat_t* out);
+int ibmgpu_csr_info(ibmgpu_mat_t m, int* rows, int* cols, int* nnz);
+int ibmgpu_csr_download(ibmgpu_ctx_t ctx, ibmgpu_mat_t m, int* rptr, int* cidx, double* val);
+int ibmgpu_csr_destroy(ibmgpu_ctx_t ctx, ibmgpu_mat_t m);
+/* SparseMatrix::spmv_into (sparse.hpp:101-110): y = A x, device pointers */
+int ibmgpu_spmv(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, const double* x_dev, double* y_dev);
+/* SparseMatrix::spmv (sparse.hpp:112-118) with host vectors (H2D, SpMV, D2H) */
+int ibmgpu_spmv_host(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, const double* x_host, double* y_host);
+/* SparseMatrix::transpose (sparse.hpp:120-138) */
+int ibmgpu_transpose(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, ibmgpu_mat_t* out);
+/* spmm (sparse.hpp:270) — Gustavson order, cancelled entries kept */
+int ibmgpu_spmm(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, ibmgpu_mat_t B, ibmgpu_mat_t* out);
+/* sliced_triple_product (sparse.hpp:282-314) */
+int ibmgpu_triple_product(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, ibmgpu_mat_t B, ibmgpu_mat_t C, int max_slice_rows,
+                          ibmgpu_mat_t* out, long long* peak_slice_nnz, int* slices);
+/* add_sparse (sparse.hpp:317-329) */
+int ibmgpu_add(ibmgpu_ctx_t ctx, double a, ibmgpu_mat_t A, double b, ibmgpu_mat_t B, ibmgpu_mat_t* out);
+/* symmetrized (sparse.hpp:351-353) */
+int ibmgpu_symmetrized(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, ibmgpu_mat_t* out);
+/* pin_row_col (operators.hpp:381-392) */
+int ibmgpu_pin(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, int pin, ibmgpu_mat_t* out);
+/* is_symmetric (sparse.hpp:331-348) */
+int ibmgpu_is_symmetric(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, double tol, int* result);
+/* scaled / scaled_rows / scaled_cols (sparse.hpp:141-161); d_host may be NULL for `scaled` */
+int ibmgpu_scale(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, int mode /*0 scalar,1 rows,2 cols*/, double a,
+                 const double* d_host, ibmgpu_mat_t* out);
+
+/* ---------------------------------------------------------------- solvers */
+/* pcg (krylov.hpp:70-136) / cg (:138). x_dev holds x0 on entry (NULL-equivalent: zeros) and x on
+ * exit. precond: IBMGPU_PC_*; hier required for IBMGPU_PC_SA. history_host (optional) receives
+ * params.max_iters+1 relative residuals at most. */
+int ibmgpu_pcg(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, int precond, ibmgpu_hier_t hier, const double* b_dev,
+               double* x_dev, const ibm_solver_params* params, ibm_solve_result* result, double* history_host);
+/* build_sa_hierarchy (amg.hpp:127-194), entirely on the device */
+int ibmgpu_sa_build(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, const ibm_sa_options* opts, ibmgpu_hier_t* out);
+int ibmgpu_sa_destroy(ibmgpu_ctx_t ctx, ibmgpu_hier_t h);
+/* sa_apply (amg.hpp:231): one V(1,1) cycle z = M^{-1} r */
+int ibmgpu_sa_apply(ibmgpu_ctx_t ctx, ibmgpu_hier_t h, const double* r_dev, double* z_dev);
+/* amg_solve (amg.hpp:250-280) */
+int ibmgpu_amg_solve(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, ibmgpu_hier_t h, const double* b_dev, double* x_dev,
+                     const ibm_solver_params* params, ibm_solve_result* result);
+/* SaHierarchy inspection (amg.hpp:33-52): levels, coarsening_stalled, coarse size */
+int ibmgpu_hier_info(ibmgpu_hier_t h, int* n_levels, int* stalled, int* coarse_rows);
+/* level l: borrowed handles (valid while h lives) and omega; l == n_levels gives coarse_A in *A */
+int ibmgpu_hier_level(ibmgpu_hier_t h, int l, ibmgpu_mat_t* A, ibmgpu_mat_t* P, ibmgpu_mat_t* Pt, double* omega);
+/* aggregate ids of level l's core rows (sa_detail::aggregate, amg.hpp:79-107); returns count */
+int ibmgpu_hier_aggregates(ibmgpu_ctx_t ctx, ibmgpu_hier_t h, int l, int* agg_host, int* n_agg);
+/* standalone strength graph + greedy aggregation (amg.hpp:110-123, :79-107) */
+int ibmgpu_aggregate(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, double theta, int n_core, int* agg_host, int* n_agg);
+
+/* ---------------------------------------------------------------- body operators */
+/* Staggered-grid description (grid.hpp:29-49). Arrays are host pointers; lengths nx+1, ny+1,
+ * nx, ny, nx, ny, nx-1, ny-1. uniform = {x0, x1, y0, y1} of the snapped uniform region. */
+typedef struct {
+    int nx, ny;
+    const double *x_faces, *y_faces, *dx, *dy, *x_c, *y_c, *del_x, *del_y;
+    double h_min;
+    double uniform[4];
+} ibm_grid_desc;
+
+/* assemble_interpolation / assemble_regularization (operators.hpp:264-342) on the device.
+ * ds: per-point arc quadrature (LagrangianBody::ds of the owning body). H may be NULL. */
+int ibmgpu_assemble_EH(ibmgpu_ctx_t ctx, const ibm_grid_desc* grid, int n_b, const double* px, const double* py,
+                       const double* ds, ibmgpu_mat_t* E, ibmgpu_mat_t* H);
+/* assemble_coupled_system (operators.hpp:408-417): Q = [G E^T], QT = Q^T, lhs2 = pin(sym(QT BN Q)) */
+int ibmgpu_coupled_system(ibmgpu_ctx_t ctx, ibmgpu_mat_t G, ibmgpu_mat_t E, ibmgpu_mat_t BN, int pin,
+                          int slice_rows, ibmgpu_mat_t* Q, ibmgpu_mat_t* QT, ibmgpu_mat_t* lhs2,
+                          long long* peak_slice_nnz);
+/* delta_roma (body.hpp:19-28), evaluated on the device for n arguments */
+int ibmgpu_delta_roma(ibmgpu_ctx_t ctx, int n, const double* r_host, double h, double* out_host);
+
+/* ---------------------------------------------------------------- case + stepper */
+/* The stepper reproduces Stepper (stepper.hpp:169-370) with every vector and operator resident in
+ * HBM. The case is read from a config file in the reference's format (config.hpp:236-355); the
+ * grid, bodies, M/L/G are assembled on the host (grid.hpp, body.hpp, operators.hpp:75-228),
+ * everything else on the device. Overrides <= 0 are ignored. */
+typedef struct {
+    double h_min;      /* grid.h_min override */
+    double dt;         /* time.dt override */
+    int n_pc;          /* stepping.n_pc override */
+    int force_rebuild; /* SteppingParams::force_rebuild */
+    int slice_rows;    /* stepping.slice_rows override */
+} ibm_case_overrides;
+
+/* StepReport (stepper.hpp:128-145) */
+typedef struct {
+    int ok;
+    int solve1_iters, solve2_iters;
+    double solve1_res, solve2_res;
+    double div_residual, noslip_residual;
+    int rebuilt_hierarchy, rebuilt_operators;
+    double bc_cfl;
+    double t_assembly, t_precond, t_explicit, t_solve1, t_solve2, t_projection; /* seconds */
+    char message[256];
+} ibm_step_report;
+
+int ibmgpu_stepper_create(ibmgpu_ctx_t ctx, const char* cfg_path, const ibm_case_overrides* ov,
+                          ibmgpu_stepper_t* out);
+int ibmgpu_stepper_destroy(ibmgpu_stepper_t st);
+/* dims: nx, ny, n_q, n_p, n_b, n_lambda, n_levels, nnz(lhs2) */
+int ibmgpu_stepper_dims(ibmgpu_stepper_t st, int* dims8);
+/* scalars: dt, nu, h_min, u_inf, ref_length, t */
+int ibmgpu_stepper_scalars(ibmgpu_stepper_t st, double* s6);
+/* Stepper::advance (stepper.hpp:231-356) */
+int ibmgpu_stepper_advance(ibmgpu_stepper_t st, ibm_step_report* rep);
+/* state download: which 0 q, 1 lambda, 2 conv_prev, 3 boundary arrays (BoundaryState order);
+ * returns the length in *n (pass out=NULL to query). */
+int ibmgpu_stepper_get(ibmgpu_stepper_t st, int which, double* out, int* n);
+/* state upload (checkpoint restore, io.hpp:112-145): same `which` codes */
+int ibmgpu_stepper_set(ibmgpu_stepper_t st, int which, const double* in, int n);
+/* compute_force_coefficients (diagnostics.hpp:26-38) on the device: out {fx, fy, cd, cl} */
+int ibmgpu_stepper_forces(ibmgpu_stepper_t st, double* out4);
+/* borrowed operator handle by name: "L","G","E","H","A","BN","Q","QT","lhs2" */
+int ibmgpu_stepper_op(ibmgpu_stepper_t st, const char* name, ibmgpu_mat_t* out);
+int ibmgpu_stepper_hier(ibmgpu_stepper_t st, ibmgpu_hier_t* out);
+/* host grid arrays (which: 0 x_faces,1 y_faces,2 dx,3 dy,4 x_c,5 y_c,6 del_x,7 del_y) */
+int ibmgpu_stepper_grid(ibmgpu_stepper_t st, int which, double* out, int* n);
+/* body points at the current time: x, y, ub_x, ub_y, ds (each n_b) */
+int ibmgpu_stepper_bodies(ibmgpu_stepper_t st, double* x, double* y, double* ubx, double* uby, double* ds);
+/* time the last advance() spent in each device phase, from CUDA events (ms) */
+int ibmgpu_stepper_phase_ms(ibmgpu_stepper_t st, float* ms6);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IBMGPU_H */

@@ -1,0 +1,182 @@
+// amg.cuh — smoothed-aggregation hierarchy on the device and the fused V(1,1) cycle.
+//
+// Reference: amg.hpp:33-52 (SaLevel/SaHierarchy), :198-225 (v_cycle). Per level l (n_l rows):
+//   K1  x = (w d) .* b ; r = b - A x           one SpMV over A_l, x gathered as (w d_j) b_j
+//   K2  b_{l+1} = P^T r                         SpMV over the explicit P^T (amg.hpp:183)
+//   ... recurse; coarsest: x_c = A_c^{-1} b_c   dense symmetric inverse GEMV (dense.hpp)
+//   K3  x += P x_{l+1}                          SpMV over P, in-place add
+//   K4  out = x + (w d) .* (b - A x)            SpMV over A_l; at level 0 the PCG's r.z partial
+//                                               is reduced in the same kernel
+// The products (w d) use the stored omega*inv_diag, which rounds exactly like the reference's
+// L.omega * L.inv_diag[i] (amg.hpp:210, :224); SELL levels therefore reproduce v_cycle bit for bit
+// up to the coarse solve.
+#pragma once
+#include <memory>
+#include <vector>
+
+#include "internal.cuh"
+#include "kern.cuh"
+
+struct ibmgpu_hier;
+
+namespace ibmgpu {
+
+struct Level {
+    Mat* A = nullptr;  // owned
+    Mat* P = nullptr;
+    Mat* Pt = nullptr;
+    double omega = 0.0;
+    int n_core = 0, n_agg = 0;
+    DBuf<double> invd, wd;  // 1/diag(A), omega/diag(A)
+    DBuf<int> agg;          // aggregate id per core row
+    DBuf<double> b, x, r, xo;  // V-cycle work vectors (b unused at level 0)
+    ~Level() {
+        delete A;
+        delete P;
+        delete Pt;
+    }
+};
+
+}  // namespace ibmgpu
+
+struct ibmgpu_hier {
+    std::vector<std::unique_ptr<ibmgpu::Level>> levels;
+    ibmgpu::Mat* coarse_A = nullptr;
+    int n_c = 0;
+    ibmgpu::DBuf<double> coarse_inv;  // n_c x n_c row-major, symmetric
+    ibmgpu::DBuf<double> cb, cx;      // coarse rhs / solution
+    bool stalled = false;
+    long long id = 0;
+    int built_at_step = -1;
+    ~ibmgpu_hier() { delete coarse_A; }
+};
+
+namespace ibmgpu {
+using Hier = ibmgpu_hier;
+
+// amg_setup.cu
+Hier* sa_build(Ctx* c, const Mat* A, const ibm_sa_options& o);
+int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& agg);
+// dense.cu
+void dense_spd_inverse(Ctx* c, const Mat* Ac, double* inv);  // factor (dense.hpp:20-40) + inverse
+void launch_dense_gemv(Ctx* c, int n, const double* Ainv, const double* x, double* y, const int* done,
+                       cudaStream_t s);
+
+// ---------------------------------------------------------------- V-cycle epilogues
+struct EpiJacobiResidual {  // K1: x_i = wd_i b_i ; r_i = b_i - s
+    static constexpr int NR = 0;
+    const double* wd;
+    const double* b;
+    double* x;
+    double* r;
+    const int* done;
+    __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ void row(int i, double s, double*) const {
+        const double bi = b[i];
+        x[i] = mul(wd[i], bi);
+        r[i] = subd(bi, s);
+    }
+    __device__ RedSlot slot() const { return {}; }
+    __device__ void fin(double*) const {}
+};
+
+struct EpiStoreSkip {  // K2: b_{l+1} = s
+    static constexpr int NR = 0;
+    double* y;
+    const int* done;
+    __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ void row(int i, double s, double*) const { y[i] = s; }
+    __device__ RedSlot slot() const { return {}; }
+    __device__ void fin(double*) const {}
+};
+
+struct EpiAddInPlace {  // K3: x_i += s
+    static constexpr int NR = 0;
+    double* x;
+    const int* done;
+    __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ void row(int i, double s, double*) const { x[i] = addd(x[i], s); }
+    __device__ RedSlot slot() const { return {}; }
+    __device__ void fin(double*) const {}
+};
+
+struct EpiPostSmooth {  // K4: out_i = x_i + wd_i (b_i - s)
+    static constexpr int NR = 0;
+    const double* wd;
+    const double* b;
+    const double* x;
+    double* out;
+    const int* done;
+    __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ void row(int i, double s, double*) const { out[i] = addd(x[i], mul(wd[i], subd(b[i], s))); }
+    __device__ RedSlot slot() const { return {}; }
+    __device__ void fin(double*) const {}
+};
+
+// K4 at level 0 with the PCG's r.z reduction fused: Fin receives tot[0] = sum r_i z_i.
+template <class Fin>
+struct EpiPostSmoothDot {
+    static constexpr int NR = 1;
+    const double* wd;
+    const double* b;  // == PCG r
+    const double* x;
+    double* out;      // == PCG z
+    const int* done;
+    RedSlot rs;
+    Fin f;
+    __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ void row(int i, double s, double* acc) const {
+        const double bi = b[i];
+        const double z = addd(x[i], mul(wd[i], subd(bi, s)));
+        out[i] = z;
+        acc[0] += bi * z;
+    }
+    __device__ RedSlot slot() const { return rs; }
+    __device__ void fin(double* tot) const { f(tot); }
+};
+
+// One V(1,1) cycle: z = M^{-1} r. `lastfin` customises the level-0 post-smooth epilogue
+// (PCG fusion); `done` (nullable) lets every kernel early-exit once a solve has finished.
+template <class LastEpi>
+inline void vcycle_launch(Ctx* c, Hier* h, const double* r_in, double* z_out, const int* done, LastEpi last,
+                          cudaStream_t s) {
+    const int L = (int)h->levels.size();
+    if (L == 0) {
+        launch_dense_gemv(c, h->n_c, h->coarse_inv.p, r_in, z_out, done, s);
+        return;
+    }
+    for (int l = 0; l < L; ++l) {
+        Level& lv = *h->levels[l];
+        const double* b = l == 0 ? r_in : lv.b.p;
+        launch_spmv(c, lv.A, XJacobi{lv.wd.p, b}, EpiJacobiResidual{lv.wd.p, b, lv.x.p, lv.r.p, done}, s);
+        double* bn = l + 1 < L ? h->levels[l + 1]->b.p : h->cb.p;
+        launch_spmv(c, lv.Pt, XPlain{lv.r.p}, EpiStoreSkip{bn, done}, s);
+    }
+    launch_dense_gemv(c, h->n_c, h->coarse_inv.p, h->cb.p, h->cx.p, done, s);
+    for (int l = L - 1; l >= 0; --l) {
+        Level& lv = *h->levels[l];
+        const double* b = l == 0 ? r_in : lv.b.p;
+        const double* ec = l + 1 < L ? h->levels[l + 1]->xo.p : h->cx.p;
+        launch_spmv(c, lv.P, XPlain{ec}, EpiAddInPlace{lv.x.p, done}, s);
+        if (l > 0) {
+            launch_spmv(c, lv.A, XPlain{lv.x.p}, EpiPostSmooth{lv.wd.p, b, lv.x.p, lv.xo.p, done}, s);
+        } else {
+            last(lv, b, z_out);
+        }
+    }
+}
+
+// Plain level-0 finish (sa_apply without a fused reduction).
+struct LastPlain {
+    Ctx* c;
+    const int* done;
+    cudaStream_t s;
+    void operator()(Level& lv, const double* b, double* z) const {
+        launch_spmv(c, lv.A, XPlain{lv.x.p}, EpiPostSmooth{lv.wd.p, b, lv.x.p, z, done}, s);
+    }
+};
+
+// kernels launched by one V-cycle (for launch accounting)
+inline int vcycle_kernels(const Hier* h) { return h->levels.empty() ? 1 : 4 * (int)h->levels.size() + 1; }
+
+}  // namespace ibmgpu

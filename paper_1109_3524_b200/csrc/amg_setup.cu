@@ -1,0 +1,454 @@
+// amg_setup.cu — build_sa_hierarchy (amg.hpp:127-194) entirely on the device.
+//
+// Per level (identical semantics and rounding to the reference):
+//   strength graph       amg.hpp:110-123  |a_ij| >= theta_l sqrt|a_ii a_jj| on the core block
+//   aggregation          amg.hpp:79-107   exact replica of the sequential 3-pass greedy:
+//                                          pass 1 is the lexicographically-first independent set of
+//                                          the conflict relation N[i] ∩ N[s] ≠ ∅ (N[x] = {x} ∪ out(x)),
+//                                          resolved by a persistent dependency-driven kernel (a node
+//                                          decides once every lower conflicting node has decided);
+//                                          pass 2 follows "first already-assigned neighbour in column
+//                                          order" chains by pointer jumping; pass 3 numbers leftovers
+//   spectral radius      amg.hpp:58-75    10 power iterations, LCG start vector by jump-ahead
+//   prolongator          amg.hpp:153-183  P_tent, DA*P_tent (ESC SpGEMM), add, identity tail, P^T
+//   Galerkin             amg.hpp:188      sliced_triple_product(P^T, A, P) on the device
+//   coarse               amg.hpp:191-192  dense SPD inverse (dense.cu)
+#include <cub/cub.cuh>
+
+#include <atomic>
+#include <cmath>
+
+#include "amg.cuh"
+#include "internal.cuh"
+#include "kern.cuh"
+
+namespace ibmgpu {
+
+namespace {
+
+inline int blocks(long long n, int b = 256) { return (int)((n + b - 1) / b); }
+
+// ---------------------------------------------------------------- strength graph
+__global__ void k_strength(int n_core, double theta, const int* __restrict__ rp, const int* __restrict__ ci,
+                           const double* __restrict__ v, const double* __restrict__ diag, int* __restrict__ cnt,
+                           const int* __restrict__ orp, int* __restrict__ oci) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_core) return;
+    int n = 0;
+    const int o = orp ? orp[i] : 0;
+    const double di = diag[i];
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int j = ci[k];
+        if (j == i || j >= n_core) continue;
+        const double bound = mul(theta, __dsqrt_rn(fabs(mul(di, diag[j]))));
+        if (fabs(v[k]) >= bound && bound > 0.0) {
+            if (oci) oci[o + n] = j;
+            ++n;
+        }
+    }
+    if (cnt) cnt[i] = n;
+}
+
+// ---------------------------------------------------------------- pass 1: LFMIS on the conflict relation
+enum : int { UNDEC = 0, SEED = 1, NOTSEED = 2 };
+
+// Persistent kernel: warps take 32-node tickets in index order. A node is NOTSEED as soon as a
+// lower conflicting node is a SEED, and SEED once every lower conflicting node is NOTSEED.
+// Lower conflicting nodes of i: s < i with s ∈ {u} ∪ in(u) for some u ∈ N[i] = {i} ∪ out(i).
+// Progress: the warp holding the globally lowest undecided node can always decide it.
+__global__ void __launch_bounds__(256) k_lfmis(int n, const int* __restrict__ srp, const int* __restrict__ sci,
+                                               const int* __restrict__ trp, const int* __restrict__ tci,
+                                               int* status, unsigned* ticket) {
+    __shared__ int wstat[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    volatile int* gstat = status;
+    for (;;) {
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(ticket, 1u);
+        t = __shfl_sync(kFull, t, 0);
+        const long long base = (long long)t * 32;
+        if (base >= n) return;
+        const int i = (int)base + lane;
+        int st = i < n ? UNDEC : NOTSEED;
+        wstat[w][lane] = st;
+        __syncwarp();
+        while (__any_sync(kFull, st == UNDEC)) {
+            if (st == UNDEC) {
+                bool pending = false, hit = false;
+                // u = i itself and u in out(i)
+                const int ob = srp[i], oe = srp[i + 1];
+                for (int q = ob - 1; q < oe && !hit; ++q) {
+                    const int u = q < ob ? i : sci[q];
+                    // candidates s = u (if u < i) and s in in(u) with s < i
+                    const int tb = trp[u], te = trp[u + 1];
+                    for (int r = tb - 1; r < te; ++r) {
+                        const int s = r < tb ? u : tci[r];
+                        if (s >= i) {
+                            if (r >= tb) break;  // in-lists are sorted: the rest are >= i
+                            continue;
+                        }
+                        const int ss = (s >= base) ? wstat[w][s - base] : gstat[s];
+                        if (ss == SEED) {
+                            hit = true;
+                            break;
+                        }
+                        if (ss == UNDEC) pending = true;
+                    }
+                }
+                if (hit)
+                    st = NOTSEED;
+                else if (!pending)
+                    st = SEED;
+                if (st != UNDEC) {
+                    gstat[i] = st;
+                    wstat[w][lane] = st;
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+__global__ void k_seed_flags(int n, const int* __restrict__ status, int* __restrict__ flag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = status[i] == SEED;
+}
+
+// seeds cover N[s]; conflict-freeness of seeds makes the writes race-free
+__global__ void k_cover(int n, const int* __restrict__ status, const int* __restrict__ seed_id,
+                        const int* __restrict__ srp, const int* __restrict__ sci, int* __restrict__ agg) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n || status[s] != SEED) return;
+    const int id = seed_id[s];
+    agg[s] = id;
+    for (int q = srp[s]; q < srp[s + 1]; ++q) agg[sci[q]] = id;
+}
+
+// pass 2 target: first out-neighbour j (column order) that is pass-1 assigned or a lower leftover
+__global__ void k_pass2_target(int n, const int* __restrict__ agg1, const int* __restrict__ srp,
+                               const int* __restrict__ sci, int* __restrict__ tgt) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (agg1[i] != -1) {
+        tgt[i] = -1;
+        return;
+    }
+    int t = -2;  // -2: no assigned neighbour (pass 3; only reachable for an asymmetric S)
+    for (int q = srp[i]; q < srp[i + 1]; ++q) {
+        const int j = sci[q];
+        if (agg1[j] != -1 || j < i) {
+            t = j;
+            break;
+        }
+    }
+    tgt[i] = t;
+}
+
+// pointer jumping along leftover chains until every target is a pass-1-assigned node. Every
+// leftover has a pass-1-assigned out-neighbour (it was not a seed, so a seed covered part of
+// N[i], and i itself is uncovered), so each lower leftover is assigned by the time i is visited.
+__global__ void k_pass2_jump(int n, const int* __restrict__ agg1, int* tgt, int* changed) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int t = tgt[i];
+    if (t < 0 || agg1[t] != -1) return;
+    const int tt = tgt[t];
+    if (tt >= 0 && tt != t) {
+        tgt[i] = tt;
+        *changed = 1;
+    }
+}
+
+__global__ void k_pass2_apply(int n, const int* __restrict__ agg1, const int* __restrict__ tgt, int* __restrict__ agg) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || agg1[i] != -1) return;
+    const int t = tgt[i];
+    agg[i] = t >= 0 ? agg1[t] : -1;
+}
+
+__global__ void k_unassigned(int n, const int* __restrict__ agg, int* __restrict__ flag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = agg[i] == -1;
+}
+
+__global__ void k_pass3(int n, int base, const int* __restrict__ flag, const int* __restrict__ pos, int* __restrict__ agg) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && flag[i]) agg[i] = base + pos[i];
+}
+
+// ---------------------------------------------------------------- prolongator pieces
+__global__ void k_agg_size(int n, const int* __restrict__ agg, int* __restrict__ size) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) atomicAdd(size + agg[i], 1);
+}
+
+// P_tent (amg.hpp:156-161): rows < n_core hold (agg[i], 1/sqrt(|agg|)); tail rows empty
+__global__ void k_ptent(int rows, int n_core, const int* __restrict__ agg, const int* __restrict__ size,
+                        int* __restrict__ rp, int* __restrict__ ci, double* __restrict__ v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > rows) return;
+    rp[i] = i < n_core ? i : n_core;
+    if (i < n_core) {
+        const int a = agg[i];
+        ci[i] = a;
+        v[i] = __ddiv_rn(1.0, __dsqrt_rn((double)size[a]));
+    }
+}
+
+__global__ void k_invd(int n, const double* __restrict__ d, double omega, double* __restrict__ invd,
+                       double* __restrict__ wd, int* __restrict__ zero) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double di = d[i];
+    if (di == 0.0) {
+        *zero = 1;
+        invd[i] = 0.0;
+    } else {
+        invd[i] = __ddiv_rn(1.0, di);
+    }
+    if (wd) wd[i] = mul(omega, invd[i]);
+}
+
+// ---------------------------------------------------------------- power iteration (amg.hpp:58-75)
+__host__ __device__ inline void lcg_compose(unsigned long long& a, unsigned long long& c, unsigned long long a2,
+                                            unsigned long long c2) {
+    // (x -> a2 (a x + c) + c2)
+    c = a2 * c + c2;
+    a = a2 * a;
+}
+
+__global__ void k_lcg_start(int n, double* __restrict__ v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    // s_{i+1} = f^{i+1}(s0), f(x) = x*A + C mod 2^64
+    unsigned long long ra = 1, rc = 0, pa = 6364136223846793005ull, pc = 1442695040888963407ull;
+    unsigned long long e = (unsigned long long)i + 1;
+    while (e) {
+        if (e & 1) lcg_compose(ra, rc, pa, pc);
+        // square: f∘f
+        const unsigned long long na = pa * pa, nc = pa * pc + pc;
+        pa = na, pc = nc;
+        e >>= 1;
+    }
+    const unsigned long long s = ra * 0x9e3779b97f4a7c15ull + rc;
+    v[i] = 0.5 + (double)(s >> 11) / (double)(1ull << 53);
+}
+
+struct PowerState {
+    double lambda;
+    int zero;
+};
+
+struct EpiPower {  // w_i = s * invd_i ; reduce w^2 ; lambda = sqrt(sum)
+    static constexpr int NR = 1;
+    const double* invd;
+    double* w;
+    RedSlot rs;
+    PowerState* ps;
+    __device__ bool skip() const { return ps->zero != 0; }
+    __device__ void row(int i, double s, double* acc) const {
+        const double wi = mul(s, invd[i]);
+        w[i] = wi;
+        acc[0] += wi * wi;
+    }
+    __device__ RedSlot slot() const { return rs; }
+    __device__ void fin(double* tot) const {
+        const double lam = __dsqrt_rn(tot[0]);
+        ps->lambda = lam;
+        if (lam == 0.0) ps->zero = 1;
+    }
+};
+
+__global__ void k_normalize(int n, const double* __restrict__ w, const PowerState* ps, double* __restrict__ v) {
+    if (ps->zero) return;
+    const double lam = ps->lambda;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = __ddiv_rn(w[i], lam);
+}
+
+double rho_dinv_a(Ctx* c, Mat* A, const double* invd, int iters) {
+    const int n = A->rows;
+    if (!A->planned) mat_plan(c, A);
+    DBuf<double> v(c, n), w(c, n);
+    DBuf<PowerState> ps(c, 1);
+    CK(cudaMemsetAsync(ps.p, 0, sizeof(PowerState), c->stream));
+    const int g = spmv_grid(A);
+    DBuf<double> part(c, (size_t)std::max(g, 1));
+    DBuf<unsigned> cnt(c, 1);
+    CK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned), c->stream));
+    k_lcg_start<<<blocks(n), 256, 0, c->stream>>>(n, v.p);
+    CK_LAUNCH(c);
+    for (int it = 0; it < iters; ++it) {
+        launch_spmv(c, A, XPlain{v.p}, EpiPower{invd, w.p, RedSlot{part.p, cnt.p}, ps.p}, c->stream);
+        k_normalize<<<elem_grid(c, n), 256, 0, c->stream>>>(n, w.p, ps.p, v.p);
+        CK_LAUNCH(c);
+    }
+    PowerState h = d2h_scalar(c, ps.p);
+    if (iters == 0) return 1.0;
+    return h.zero ? 1.0 : h.lambda;
+}
+
+}  // namespace
+
+// Strength graph + exact greedy aggregation; returns aggregate count, agg sized n_core.
+int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& agg) {
+    agg.alloc(c, (size_t)std::max(n_core, 1));
+    if (n_core == 0) return 0;
+    DBuf<double> diag(c, (size_t)A->rows);
+    diag_of(c, A, diag.p);
+    // S (pattern only)
+    DBuf<int> cnt(c, (size_t)n_core + 1);
+    Mat S;
+    S.rows = S.cols = n_core;
+    S.rp.alloc(c, (size_t)n_core + 1);
+    k_strength<<<blocks(n_core), 256, 0, c->stream>>>(n_core, theta, A->rp.p, A->ci.p, A->v.p, diag.p, cnt.p, nullptr,
+                                                      nullptr);
+    CK_LAUNCH(c);
+    exclusive_scan_total(c, cnt.p, S.rp.p, n_core);
+    S.nnz = d2h_scalar(c, S.rp.p + n_core);
+    S.ci.alloc(c, (size_t)S.nnz);
+    S.v.alloc(c, (size_t)S.nnz);
+    CK(cudaMemsetAsync(S.v.p, 0, sizeof(double) * (size_t)S.nnz, c->stream));
+    k_strength<<<blocks(n_core), 256, 0, c->stream>>>(n_core, theta, A->rp.p, A->ci.p, A->v.p, diag.p, nullptr,
+                                                      S.rp.p, S.ci.p);
+    CK_LAUNCH(c);
+    Mat* St = transpose(c, &S);  // in-neighbour lists (sorted by source row)
+
+    // pass 1
+    DBuf<int> status(c, (size_t)n_core), seedflag(c, (size_t)n_core), seed_id(c, (size_t)n_core + 1);
+    DBuf<unsigned> ticket(c, 1);
+    CK(cudaMemsetAsync(status.p, 0, sizeof(int) * (size_t)n_core, c->stream));
+    CK(cudaMemsetAsync(ticket.p, 0, sizeof(unsigned), c->stream));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lfmis, 256, 0));
+    const int grid = std::max(1, std::min(per_sm * c->num_sms, (n_core + 255) / 256));
+    k_lfmis<<<grid, 256, 0, c->stream>>>(n_core, S.rp.p, S.ci.p, St->rp.p, St->ci.p, status.p, ticket.p);
+    CK_LAUNCH(c);
+    k_seed_flags<<<blocks(n_core), 256, 0, c->stream>>>(n_core, status.p, seedflag.p);
+    CK_LAUNCH(c);
+    exclusive_scan_total(c, seedflag.p, seed_id.p, n_core);
+    const int n_seeds = d2h_scalar(c, seed_id.p + n_core);
+    DBuf<int> agg1(c, (size_t)n_core);
+    CK(cudaMemsetAsync(agg1.p, 0xff, sizeof(int) * (size_t)n_core, c->stream));
+    k_cover<<<blocks(n_core), 256, 0, c->stream>>>(n_core, status.p, seed_id.p, S.rp.p, S.ci.p, agg1.p);
+    CK_LAUNCH(c);
+
+    // pass 2: pointer jumping over "first assigned neighbour" chains
+    DBuf<int> tgt(c, (size_t)n_core), changed(c, 1);
+    k_pass2_target<<<blocks(n_core), 256, 0, c->stream>>>(n_core, agg1.p, S.rp.p, S.ci.p, tgt.p);
+    CK_LAUNCH(c);
+    for (int round = 0; round < 64; ++round) {
+        CK(cudaMemsetAsync(changed.p, 0, sizeof(int), c->stream));
+        k_pass2_jump<<<blocks(n_core), 256, 0, c->stream>>>(n_core, agg1.p, tgt.p, changed.p);
+        CK_LAUNCH(c);
+        if (!d2h_scalar(c, changed.p)) break;
+    }
+    d2d(c, agg.p, agg1.p, (size_t)n_core);
+    k_pass2_apply<<<blocks(n_core), 256, 0, c->stream>>>(n_core, agg1.p, tgt.p, agg.p);
+    CK_LAUNCH(c);
+
+    // pass 3: leftovers numbered after the seeds in index order
+    DBuf<int> flag(c, (size_t)n_core), pos(c, (size_t)n_core + 1);
+    k_unassigned<<<blocks(n_core), 256, 0, c->stream>>>(n_core, agg.p, flag.p);
+    CK_LAUNCH(c);
+    exclusive_scan_total(c, flag.p, pos.p, n_core);
+    const int n3 = d2h_scalar(c, pos.p + n_core);
+    if (n3) {
+        k_pass3<<<blocks(n_core), 256, 0, c->stream>>>(n_core, n_seeds, flag.p, pos.p, agg.p);
+        CK_LAUNCH(c);
+    }
+    delete St;
+    return n_seeds + n3;
+}
+
+Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
+    require(A_fine->rows == A_fine->cols, "sa: square matrix required");
+    static std::atomic<long long> next_id{1};
+    auto* h = new Hier();
+    h->id = next_id++;
+    try {
+        const int tail = std::min(o.keep_fine_tail, A_fine->rows);
+        // level-0 A is a private copy (the hierarchy owns every level, as SaLevel::A does)
+        Mat* A = scale(c, A_fine, 0, 1.0, nullptr);
+        for (int lev = 0; lev < o.max_levels && A->rows > o.max_coarse + tail; ++lev) {
+            const double theta_l = o.theta * std::pow(0.5, lev);
+            const int n_core = A->rows - tail;
+            auto L = std::make_unique<Level>();
+            const int n_agg = aggregate_device(c, A, theta_l, n_core, L->agg);
+            if (n_agg >= n_core) {
+                h->stalled = true;
+                break;
+            }
+            const int n = A->rows;
+            DBuf<double> d(c, (size_t)n);
+            diag_of(c, A, d.p);
+            L->invd.alloc(c, (size_t)n);
+            DBuf<int> zero(c, 1);
+            CK(cudaMemsetAsync(zero.p, 0, sizeof(int), c->stream));
+            k_invd<<<blocks(n), 256, 0, c->stream>>>(n, d.p, 0.0, L->invd.p, nullptr, zero.p);
+            CK_LAUNCH(c);
+            if (d2h_scalar(c, zero.p)) {
+                delete A;
+                fail(IBMGPU_EINVAL, "sa: zero diagonal");
+            }
+            const double rho = rho_dinv_a(c, A, L->invd.p, o.power_iterations);
+            const double omega = (4.0 / 3.0) / rho;
+            L->wd.alloc(c, (size_t)n);
+            k_invd<<<blocks(n), 256, 0, c->stream>>>(n, d.p, omega, L->invd.p, L->wd.p, zero.p);
+            CK_LAUNCH(c);
+
+            // tentative prolongator
+            DBuf<int> size(c, (size_t)n_agg);
+            CK(cudaMemsetAsync(size.p, 0, sizeof(int) * (size_t)n_agg, c->stream));
+            k_agg_size<<<blocks(n_core), 256, 0, c->stream>>>(n_core, L->agg.p, size.p);
+            CK_LAUNCH(c);
+            Mat* Ptent = mat_new(c, n, n_agg, n_core);
+            k_ptent<<<blocks(n + 1), 256, 0, c->stream>>>(n, n_core, L->agg.p, size.p, Ptent->rp.p, Ptent->ci.p,
+                                                          Ptent->v.p);
+            CK_LAUNCH(c);
+            // P = (I - omega D^{-1} A) P_tent on the core; identity on the tail
+            Mat* DA = scale(c, A, 1, 0.0, L->invd.p);
+            Mat* DAP = spmm_rows(c, DA, 0, DA->rows, Ptent);
+            delete DA;
+            Mat* Pcore = add(c, 1.0, Ptent, -omega, DAP);
+            delete DAP;
+            delete Ptent;
+            Mat* P = tail > 0 ? identity_tail_append(c, Pcore, n_core, n_agg, tail) : Pcore;
+            if (tail > 0) delete Pcore;
+            Mat* Pt = transpose(c, P);
+            Mat* Ac = triple_product(c, Pt, A, P, std::max(1, Pt->rows), nullptr, nullptr);
+
+            L->A = A;
+            L->P = P;
+            L->Pt = Pt;
+            L->omega = omega;
+            L->n_core = n_core;
+            L->n_agg = n_agg;
+            h->levels.push_back(std::move(L));
+            A = Ac;
+        }
+        h->coarse_A = A;
+        h->n_c = A->rows;
+        // V-cycle plans + work vectors
+        for (size_t l = 0; l < h->levels.size(); ++l) {
+            Level& lv = *h->levels[l];
+            for (Mat* m : {lv.A, lv.P, lv.Pt})
+                if (!m->planned) mat_plan(c, m);
+            const size_t n = (size_t)lv.A->rows;
+            if (l > 0) lv.b.alloc(c, n);
+            lv.x.alloc(c, n);
+            lv.r.alloc(c, n);
+            lv.xo.alloc(c, n);
+        }
+        h->coarse_inv.alloc(c, (size_t)h->n_c * h->n_c);
+        dense_spd_inverse(c, h->coarse_A, h->coarse_inv.p);
+        h->cb.alloc(c, (size_t)h->n_c);
+        h->cx.alloc(c, (size_t)h->n_c);
+        sync(c);
+    } catch (...) {
+        delete h;
+        throw;
+    }
+    return h;
+}
+
+}  // namespace ibmgpu

@@ -1,0 +1,167 @@
+// internal.cuh — shared internals of libibmgpu (context, memory, device CSR, errors).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ibmgpu.h"
+
+namespace ibmgpu {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+inline void require(bool ok, const std::string& msg) {
+    if (!ok) fail(IBMGPU_EINVAL, msg);
+}
+
+#define CK(call)                                                                                        \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess)                                                                          \
+            ::ibmgpu::fail(e_ == cudaErrorMemoryAllocation ? IBMGPU_ENOMEM : IBMGPU_ECUDA,               \
+                           std::string(#call) + ": " + cudaGetErrorString(e_) + " (" + __FILE__ + ":" +   \
+                               std::to_string(__LINE__) + ")");                                         \
+    } while (0)
+
+#define CK_LAUNCH(ctx)                 \
+    do {                               \
+        CK(cudaGetLastError());        \
+        ++(ctx)->launches;             \
+    } while (0)
+
+}  // namespace ibmgpu
+
+struct ibmgpu_ctx {
+    int device = 0;
+    int nranks = 1, rank = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    std::string err;
+    long long launches = 0;
+    int num_sms = 148;
+    void* nccl = nullptr;       // ncclComm_t when nranks > 1
+    void* pcg_cache = nullptr;  // pcg.cu plan cache
+};
+
+namespace ibmgpu {
+
+using Ctx = ibmgpu_ctx;
+
+// Stream-ordered device buffer (cudaMallocAsync on the context's pool).
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    DBuf() = default;
+    DBuf(Ctx* c, size_t count) { alloc(c, count); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr, o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p, n = o.n, s = o.s;
+            o.p = nullptr, o.n = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(Ctx* c, size_t count) {
+        release();
+        s = c->stream;
+        n = count;
+        if (count) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, s));
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    T* get() const { return p; }
+    operator T*() const { return p; }
+};
+
+template <class T>
+inline void h2d(Ctx* c, T* dst, const T* src, size_t n) {
+    if (n) CK(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyHostToDevice, c->stream));
+}
+template <class T>
+inline void d2h(Ctx* c, T* dst, const T* src, size_t n) {
+    if (n) CK(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyDeviceToHost, c->stream));
+}
+template <class T>
+inline void d2d(Ctx* c, T* dst, const T* src, size_t n) {
+    if (n) CK(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyDeviceToDevice, c->stream));
+}
+inline void sync(Ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
+
+template <class T>
+inline T d2h_scalar(Ctx* c, const T* src) {
+    T v;
+    d2h(c, &v, src, 1);
+    sync(c);
+    return v;
+}
+
+// SpMV execution plan chosen at construction from the row-length profile.
+enum SpmvKind { SPMV_SELL = 0, SPMV_VECTOR = 1 };
+
+}  // namespace ibmgpu
+
+// Device CSR (sparse.hpp:214-219 layout: int32 row_ptr/col_idx, f64 values) plus the
+// SpMV-side SELL-32 copy (column-major within 32-row slices, padded to the slice width).
+struct ibmgpu_mat {
+    int rows = 0, cols = 0, nnz = 0;
+    ibmgpu::DBuf<int> rp, ci;
+    ibmgpu::DBuf<double> v;
+    // SpMV plan
+    int kind = ibmgpu::SPMV_SELL;
+    int tpr = 1;  // threads per row (vector kind)
+    int max_row = 0;
+    ibmgpu::DBuf<int> sell_off;  // n_slices + 1 element offsets
+    ibmgpu::DBuf<int> sell_ci;
+    ibmgpu::DBuf<double> sell_v;
+    bool planned = false;
+    bool borrowed = false;  // owned by a hierarchy / stepper; ibmgpu_csr_destroy refuses
+};
+
+namespace ibmgpu {
+using Mat = ibmgpu_mat;
+
+// csr.cu
+Mat* mat_new(Ctx* c, int rows, int cols, int nnz);
+void mat_plan(Ctx* c, Mat* m);              // build the SpMV plan (SELL copy or vector width)
+void spmv(Ctx* c, Mat* A, const double* x, double* y);
+Mat* mat_upload(Ctx* c, int rows, int cols, int nnz, const int* rp, const int* ci, const double* v);
+void mat_download(Ctx* c, const Mat* m, int* rp, int* ci, double* v);
+void diag_of(Ctx* c, const Mat* A, double* d);  // (*this)(i,i) by binary search (sparse.hpp:163)
+double max_abs(Ctx* c, const Mat* A);
+
+// sparse_ops.cu
+Mat* transpose(Ctx* c, const Mat* A);
+Mat* spmm_rows(Ctx* c, const Mat* A, int r0, int r1, const Mat* B);
+Mat* triple_product(Ctx* c, const Mat* A, const Mat* B, const Mat* C, int slice, long long* peak, int* slices);
+Mat* add(Ctx* c, double a, const Mat* A, double b, const Mat* B);
+Mat* symmetrized(Ctx* c, const Mat* A);
+Mat* pin(Ctx* c, const Mat* A, int p);
+Mat* scale(Ctx* c, const Mat* A, int mode, double a, const double* d_dev);
+Mat* from_triplets(Ctx* c, int rows, int cols, size_t n, const int* r_dev, const int* c_dev, const double* v_dev);
+Mat* concat_cols(Ctx* c, const Mat* G, const Mat* Et);
+Mat* identity_tail_append(Ctx* c, const Mat* Pcore, int n_core, int n_agg, int tail);
+bool is_symmetric(Ctx* c, const Mat* A, double tol);
+Mat* diag_matrix(Ctx* c, int n, const double* d_dev);
+
+// scan helper (cub) — exclusive scan of n ints into out (n+1 entries, out[n] = total)
+void exclusive_scan_total(Ctx* c, const int* in, int* out, int n);
+long long exclusive_scan_total64(Ctx* c, const long long* in, long long* out, int n);
+
+}  // namespace ibmgpu

@@ -1,0 +1,199 @@
+"""GPU parity: PCG (identity / diagonal / SA), the device-built SA hierarchy and the V-cycle vs the
+C restatement and the golden fixtures. Contract (BASELINE north_star): iterations within ±2,
+solutions within 1e-6 relative at the reference tolerance; SA structure bit-exact."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1109_3524_b200 import ibm
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(m):
+    return ibm.SparseMatrix.from_host(m)
+
+
+def test_cg_identity_one_iteration():
+    I = ibm.SparseMatrix.identity(6)
+    b = np.linspace(-1, 1, 6)
+    r = ibm.cg(I, b, None, ibm.SolverParams())
+    assert r.converged() and r.iterations <= 1 and np.allclose(r.x, b, atol=1e-12)
+
+
+def test_cg_matches_lu():
+    A = O.poisson1d(4)
+    r = ibm.cg(dev(A), [1.0, 0, 0, 0], None, ibm.SolverParams(rel_tol=1e-12))
+    assert r.converged()
+    assert np.allclose(r.x, np.linalg.solve(A.dense(), [1.0, 0, 0, 0]), atol=1e-10)
+
+
+def test_breakdown_zero_rhs_and_errors():
+    A = ibm.SparseMatrix.from_triplets(2, 2, [(0, 0, 1.0), (1, 1, -1.0)])
+    assert ibm.cg(A, [0.0, 1.0], None, ibm.SolverParams()).status == ibm.BREAKDOWN
+    P = dev(O.poisson5(5))
+    r = ibm.pcg(P, np.zeros(25), np.ones(25), ibm.DiagonalPreconditioner(P), ibm.SolverParams())
+    assert r.converged() and not r.x.any()
+    N = ibm.SparseMatrix.from_triplets(2, 2, [(0, 0, 2.0), (0, 1, 1.0), (1, 1, 2.0)])
+    with pytest.raises(ValueError):
+        ibm.cg(N, [1.0, 1.0], None, ibm.SolverParams(check_symmetry=True))
+    Z = ibm.SparseMatrix.from_triplets(2, 2, [(0, 0, 1.0), (0, 1, 1.0), (1, 0, 1.0)])
+    with pytest.raises(ValueError):
+        ibm.pcg(Z, [1.0, 1.0], None, ibm.DiagonalPreconditioner(Z), ibm.SolverParams())
+    with pytest.raises(ValueError):
+        ibm.pcg(P, np.ones(25), None, ibm.IdentityPreconditioner(), ibm.SolverParams(rel_tol=0.0))
+
+
+def test_max_iterations_status():
+    P = dev(O.poisson5(30))
+    r = ibm.cg(P, np.ones(900), None, ibm.SolverParams(max_iters=3, record_history=True))
+    assert r.status == ibm.MAX_ITERATIONS and r.iterations == 3 and len(r.history) == 4
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_pcg_matches_oracle(port, kind):
+    A = O.poisson5(40)
+    b = np.sin(np.arange(A.rows) * 1.3)
+    x0 = np.cos(np.arange(A.rows))
+    M = ibm.IdentityPreconditioner() if kind == 0 else ibm.DiagonalPreconditioner(None)
+    r = ibm.pcg(dev(A), b, x0, M, ibm.SolverParams(rel_tol=1e-8, record_history=True))
+    o = port.pcg(A, b, x0=x0, kind=kind, rel_tol=1e-8, history=True)
+    assert abs(r.iterations - o["iterations"]) <= 2
+    assert np.max(np.abs(r.x - o["x"])) <= 1e-6 * np.max(np.abs(o["x"]))
+    n = min(len(r.history), len(o["history"]))
+    assert np.allclose(r.history[:n], o["history"][:n], rtol=1e-6)
+
+
+def _hier_equal(h_dev: "ibm.SaHierarchy", h_port, n_b: int):
+    nl, stalled, nc = h_dev.info()
+    assert nl == h_port.n_levels and stalled == h_port.stalled
+    for l in range(nl):
+        Ld, Lp = h_dev.level(l), h_port.level(l)
+        for k in ("A", "P", "Pt"):
+            H.assert_csr_equal(H.dev_to_csr(Ld[k]), Lp[k])
+        assert Ld["omega"] == pytest.approx(Lp["omega"], rel=1e-12)
+    H.assert_csr_equal(H.dev_to_csr(h_dev.coarse_A()), h_port.coarse())
+
+
+def test_sa_hierarchy_bitwise_poisson(port):
+    for n in (8, 20, 64):
+        A = O.poisson5(n)
+        hd = ibm.build_sa_hierarchy(dev(A))
+        hp = port.sa_build(A)
+        _hier_equal(hd, hp, 0)
+        gold = H.hashes()[f"poisson5_{n}"]
+        for l, gl in enumerate(gold["levels"]):
+            m = H.dev_to_csr(hd.level(l)["A"])
+            assert H.csr_hash(m) == (gl["A"]["struct"], gl["A"]["values"])
+
+
+def test_sa_hierarchy_bitwise_small_case(port):
+    d = H.small()
+    lhs2 = H.small_mat(d, "lhs2")
+    n_b = int(d["dims"][4])
+    hd = ibm.build_sa_hierarchy(dev(lhs2), ibm.SaOptions(keep_fine_tail=2 * n_b))
+    hp = port.sa_build(lhs2, tail=2 * n_b)
+    _hier_equal(hd, hp, n_b)
+    for l in range(hd.n_levels):
+        n_agg, agg = hd.aggregates(l)
+        n_core = hd.level(l)["A"].rows() - 2 * n_b
+        assert np.array_equal(agg[:n_core], d[f"L{l}_agg"])
+
+
+@pytest.mark.parametrize("name", ["cavity", "cylinder_re40_smoke", "flapping_smoke", "cylinder_re40"])
+def test_aggregation_matches_golden(ref, name):
+    """Device greedy aggregation == sa_detail::aggregate on every level of the reference hierarchy."""
+    gold = H.hashes()[name]
+    c = ref.case(H.case(name))
+    h = c.hierarchy()
+    for l, gl in enumerate(gold["levels"]):
+        A = h.level(l)["A"]
+        n_core = A.rows - 2 * c.n_b
+        agg = np.zeros(max(n_core, 1), np.int32)
+        import ctypes as C
+        Ad = dev(A)
+        n = C.c_int()
+        Ad.ctx.check(Ad.ctx.lib.ibmgpu_aggregate(Ad.ctx.h, Ad.h, 0.25 * 0.5 ** l, n_core,
+                                                 agg.ctypes.data_as(C.POINTER(C.c_int)), C.byref(n)))
+        assert n.value == gl["n_agg"]
+        assert hashlib.sha256(np.ascontiguousarray(agg[:n_core], np.int32).tobytes()).hexdigest() == gl["agg"]
+
+
+def test_vcycle_matches_oracle_and_is_self_adjoint():
+    d = H.small()
+    lhs2 = H.small_mat(d, "lhs2")
+    n_b = int(d["dims"][4])
+    hd = ibm.build_sa_hierarchy(dev(lhs2), ibm.SaOptions(keep_fine_tail=2 * n_b))
+    z = ibm.sa_apply(hd, d["bench_b"])
+    assert np.max(np.abs(z - d["vcycle_z"])) <= 1e-10 * np.max(np.abs(d["vcycle_z"]))
+    A = O.poisson5(20)
+    h = ibm.build_sa_hierarchy(dev(A))
+    rng = np.random.default_rng(21)
+    r1, r2 = rng.uniform(-1, 1, A.rows), rng.uniform(-1, 1, A.rows)
+    z1, z2, zs = ibm.sa_apply(h, r1), ibm.sa_apply(h, r2), ibm.sa_apply(h, r1 + r2)
+    assert np.max(np.abs(zs - z1 - z2)) <= 1e-10 * np.linalg.norm(zs)
+    assert abs(z1 @ r2 - r1 @ z2) <= 1e-10 * abs(r1 @ z2)
+
+
+def test_pcg_sa_matches_golden_small_case():
+    d = H.small()
+    lhs2 = H.small_mat(d, "lhs2")
+    n_b = int(d["dims"][4])
+    A = dev(lhs2)
+    hd = ibm.build_sa_hierarchy(A, ibm.SaOptions(keep_fine_tail=2 * n_b))
+    r = ibm.pcg(A, d["bench_b"], None, ibm.SaPreconditioner(hd), ibm.SolverParams(record_history=True))
+    assert r.converged()
+    assert abs(r.iterations - int(d["bench_iters"][0])) <= 2
+    assert np.max(np.abs(r.x - d["bench_x"])) <= 1e-6 * np.max(np.abs(d["bench_x"]))
+
+
+def test_iteration_bounds_poisson64():
+    A = O.poisson5(64)
+    b = np.random.default_rng(33).uniform(-1, 1, A.rows)
+    Ad = dev(A)
+    p = ibm.SolverParams()
+    plain = ibm.cg(Ad, b, None, p)
+    diag = ibm.pcg(Ad, b, None, ibm.DiagonalPreconditioner(Ad), p)
+    sa = ibm.pcg(Ad, b, None, ibm.SaPreconditioner(ibm.build_sa_hierarchy(Ad)), p)
+    assert plain.iterations <= 300 and diag.iterations <= plain.iterations
+    assert sa.iterations < plain.iterations / 4
+    for r in (plain, diag, sa):
+        assert np.linalg.norm(b - A.spmv_np(r.x) if False else b - Ad.spmv(r.x)) / np.linalg.norm(b) <= 1e-5
+
+
+def test_amg_solve_contract():
+    A = O.poisson5(32)
+    Ad = dev(A)
+    b = np.random.default_rng(41).uniform(-1, 1, A.rows)
+    h = ibm.build_sa_hierarchy(Ad)
+    r = ibm.amg_solve(Ad, h, b, None, ibm.SolverParams(max_iters=200))
+    assert r.converged()
+    assert np.linalg.norm(b - Ad.spmv(r.x)) / np.linalg.norm(b) <= 1e-5
+
+
+def test_identity_hierarchy_single_level():
+    h = ibm.build_sa_hierarchy(ibm.SparseMatrix.identity(10))
+    assert h.n_levels == 0 and h.level_count() == 1
+    z = ibm.sa_apply(h, np.full(10, 3.0))
+    assert np.allclose(z, 3.0, rtol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["cylinder_re40_smoke", "cylinder_re40"])
+def test_pcg_sa_case_iterations(ref, name):
+    gold = H.hashes()[name]
+    c = ref.case(H.case(name))
+    L2 = c.op("lhs2")
+    A = dev(L2)
+    h = ibm.build_sa_hierarchy(A, ibm.SaOptions(keep_fine_tail=2 * c.n_b))
+    for l, gl in enumerate(gold["levels"]):
+        m = H.dev_to_csr(h.level(l)["A"])
+        assert H.csr_hash(m) == (gl["A"]["struct"], gl["A"]["values"]), l
+    b = H.bench_rhs(A.spmv, L2.rows)
+    r = ibm.pcg(A, b, None, ibm.SaPreconditioner(h), ibm.SolverParams())
+    assert r.converged()
+    assert abs(r.iterations - gold["bench_pcg_sa"]["iterations"]) <= 2
+    rd = ibm.pcg(A, b, None, ibm.DiagonalPreconditioner(A), ibm.SolverParams())
+    assert abs(rd.iterations - gold["bench_pcg_diag"]["iterations"]) <= 2
