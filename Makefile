@@ -8,14 +8,17 @@ HOST := $(wildcard $(PKG)/csrc/host/*.cpp)
 HDR := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/host/*.hpp) include/ibmgpu.h
 OBJDIR := build/obj
 OBJ := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(SRC)) $(patsubst $(PKG)/csrc/host/%.cpp,$(OBJDIR)/host_%.o,$(HOST))
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fopenmp -Xptxas -v --expt-relaxed-constexpr
-HOSTFLAGS := -O3 -std=c++17 -fPIC -fopenmp -ffp-contract=off
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC,-fopenmp -Xptxas -v --expt-relaxed-constexpr
+HOSTFLAGS := -O3 -std=c++20 -fPIC -fopenmp -ffp-contract=off
 
 all: $(PKG)/libibmgpu.so oracle
 
+# the stepper's explicit-term kernels must round like the reference (no FMA contraction)
+$(OBJDIR)/stepper.o: NVEXTRA := --fmad=false
+
 $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p $(OBJDIR)
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) $(NVEXTRA) -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
 
 $(OBJDIR)/host_%.o: $(PKG)/csrc/host/%.cpp $(HDR)
 	@mkdir -p $(OBJDIR)

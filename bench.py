@@ -1,0 +1,359 @@
+"""Benchmark: IBPM time steps/s on the B200 hot path (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|s4m|c2a|cavity|flapping|c5-N]
+                  [--impl ours|reference]
+
+A "step" is one Stepper::advance (stepper.hpp:231-356): explicit terms, PCG-diag momentum solve,
+SA-PCG coupled solve, projection and invariants, all resident in HBM (device-built operators and
+SA hierarchy). Prints ONE JSON line (rank 0). Default workload: C2 = impulsively started cylinder,
+Re 40, ~1M cells (cylinder_re40.cfg at h_min 0.002 -> 1042^2), BASELINE.json configs[1]; the
+S-4M (configs[2]) per-iteration roofline is reported alongside under "s4m" unless --no-s4m.
+
+--impl reference runs the reference's own CPU implementation (oracle/_ref/libibmref.so, the
+unmodified reference headers) on the same case with all host threads; it never touches the GPU.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+CASES = os.path.join(ROOT, "cases")
+
+WORKLOADS = {
+    # name: (cfg, h_min override, dt override, description)
+    "c2": ("cylinder_re40", 0.002, 0.001, "Re40 impulsively started cylinder, h_min 0.002 (1042^2, ~1.09M-row lhs2)"),
+    "s4m": ("cylinder_re3000", 0.001, 2.5e-4, "Re3000 cylinder geometry, h_min 0.001 (2040^2, 4.17M-row lhs2)"),
+    "c2a": ("cylinder_re40", 0.0, 0.0, "Re40 cylinder 330^2 (reference cfg)"),
+    "cavity": ("cavity", 0.0, 0.0, "lid-driven cavity Re100 128^2, no body"),
+    "flapping": ("flapping", 0.0, 0.0, "flapping ellipse 930x654, moving body (lhs2 rebuilt every step)"),
+}
+
+
+def workload(name: str):
+    if name.startswith("c5-"):
+        N = int(name[3:])
+        h = 30.72 / N
+        return ("uniform_cylinder", h, 0.5 * h, f"synthetic uniform cylinder {N}^2")
+    return WORKLOADS[name]
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm = [float(r[0]) for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 8:
+                for k, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(k)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- algorithmic bytes
+def spmv_bytes(rows, cols, nnz):
+    """12 nnz + 4 (rows+1) + 8 cols + 8 rows."""
+    return 12 * nnz + 4 * (rows + 1) + 8 * cols + 8 * rows
+
+
+def hier_bytes(h) -> tuple[float, dict]:
+    """B_it2 of one solve-2 SA-PCG iteration."""
+    nl, _, nc = h.info()
+    L0 = h.level(0)["A"] if nl else h.coarse_A()
+    n0, nnz0 = L0.rows(), L0.nnz()
+    b = 12 * nnz0 + 92 * n0
+    levels = []
+    for l in range(nl):
+        lv = h.level(l)
+        A, P = lv["A"], lv["P"]
+        n_l, n_next = A.rows(), P.cols()
+        b += 24 * A.nnz() + 24 * P.nnz() + 100 * n_l + 20 * n_next
+        levels.append(dict(rows=n_l, nnz_A=A.nnz(), nnz_P=P.nnz()))
+    b += 8 * nc * nc + 16 * nc
+    return float(b), dict(levels=levels, n_c=nc)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, rank: int, world: int):
+    import numpy as np
+
+    from paper_1109_3524_b200 import ibm
+
+    cfg, h_min, dt, desc = workload(args.workload)
+    ctx = ibm.Context(int(os.environ.get("LOCAL_RANK", "0")))
+    t0 = time.time()
+    st = ibm.Stepper(os.path.join(CASES, cfg + ".cfg"), h_min=h_min, dt=dt, ctx=ctx)
+    setup_s = time.time() - t0
+    h = st.hierarchy()
+    b_it2, hinfo = hier_bytes(h)
+    A = st.op("A")
+    b_it1 = 12 * A.nnz() + 108 * st.n_q
+    Lm, QT, Q, BN = st.op("L"), st.op("QT"), st.op("Q"), st.op("BN")
+    b_fixed = (spmv_bytes(Lm.rows(), Lm.cols(), Lm.nnz()) + 2 * spmv_bytes(QT.rows(), QT.cols(), QT.nnz())
+               + spmv_bytes(Q.rows(), Q.cols(), Q.nnz()) + spmv_bytes(BN.rows(), BN.cols(), BN.nnz())
+               + 48 * st.n_q)
+
+    for _ in range(args.warmup):
+        r = st.advance()
+        if not r.ok:
+            raise RuntimeError(r.message)
+    launches0 = ctx.launches()
+    reps = []
+    solve2_ms = []
+    # ---- device-timed region (inputs resident in HBM): K steps bracketed by events
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        ctx.sync()
+        ctx.timer_start()
+        for _ in range(args.steps):
+            r = st.advance()
+            if not r.ok:
+                raise RuntimeError(r.message)
+            reps.append(r)
+            solve2_ms.append(st.phase_ms()["solve2"])
+        dev_ms = ctx.timer_stop()
+        launches = ctx.launches() - launches0
+        # ---- end-to-end through the C-ABI: per step the host uploads body kinematics and reads
+        #      back the report, the forces and f~ (host buffers, copies inside the timed region)
+        t1 = time.perf_counter()
+        for _ in range(args.steps):
+            r = st.advance()
+            if not r.ok:
+                raise RuntimeError(r.message)
+            st.forces()
+            if st.n_b:
+                lam = st.get("lambda")  # f~ lives at the tail of lambda
+                _ = lam[st.n_p:]
+        e2e_s = time.perf_counter() - t1
+    clocks = clk.summary()
+
+    K = args.steps
+    its2 = [r.solve2_iters for r in reps]
+    its1 = [r.solve1_iters for r in reps]
+    steps_per_s = K / (dev_ms * 1e-3)
+    # dominant launch: the solve-2 SA-PCG graph (89-99% of the step); algorithmic bytes per launch
+    s2_ms = sum(solve2_ms) / K
+    s2_bytes = sum(its2) / K * b_it2 + spmv_bytes(st.n_lambda, st.n_lambda, st.nnz_lhs2)
+    peak, peak_kind = load_peaks()
+    achieved = s2_bytes / (s2_ms * 1e-3) / 1e9
+    b_step = sum(its1) / K * b_it1 + sum(its2) / K * b_it2 + b_fixed
+    n_b = st.n_b
+    h2d = 5 * 8 * n_b
+    d2h = 8 * (st.n_lambda) + 32 + 2 * 96
+    out = {
+        "metric": "time steps/sec (IBPM step: explicit + PCG-diag + SA-PCG + projection)",
+        "value": round(steps_per_s * world, 4),
+        "unit": "steps/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": round(dev_ms / K, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (deterministic case file; no datasets)",
+        "config": {"workload": args.workload, "case": cfg + ".cfg", "h_min": h_min or None, "dt": dt or None,
+                   "desc": desc, "grid": [st.nx, st.ny], "n_lambda": st.n_lambda, "nnz_lhs2": st.nnz_lhs2,
+                   "n_b": n_b, "sa_levels": len(hinfo["levels"]), "n_c": hinfo["n_c"],
+                   "parallelism": "replicas" if world > 1 else "single-gpu",
+                   "l2": "inputs larger than L2 (per-iteration working set >> 126 MB)" if b_it2 > 5e8 else
+                   "working set partly L2-resident"},
+        "cg_iters_per_step": round(sum(its2) / K, 2),
+        "momentum_iters_per_step": round(sum(its1) / K, 2),
+        "cg_iters_per_s": round(sum(its2) / (sum(solve2_ms) * 1e-3), 1),
+        "cg_iteration_ms": round(s2_ms / max(sum(its2) / K, 1), 4),
+        "setup_s": round(setup_s, 3),
+        "step_hbm_gbs": round(b_step / (dev_ms / K * 1e-3) / 1e9, 1),
+        "roofline": {"kernel": "solve-2 SA-PCG graph launch (SpMV + V-cycle + fused reductions)",
+                     "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "frac_of_8tbs": round(achieved / 8000, 4),
+                     "bytes_per_launch": s2_bytes, "b_it2": b_it2, "traffic": None},
+        "e2e": {"value": round(K / e2e_s * world, 4), "unit": "steps/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    return out, st
+
+
+def s4m_probe(args) -> dict:
+    """S-4M per-iteration roofline (north-star target: >= 60% of HBM roofline per CG iteration)."""
+    from paper_1109_3524_b200 import ibm
+    cfg, h_min, dt, desc = WORKLOADS["s4m"]
+    t0 = time.time()
+    st = ibm.Stepper(os.path.join(CASES, cfg + ".cfg"), h_min=h_min, dt=dt)
+    setup = time.time() - t0
+    b_it2, hinfo = hier_bytes(st.hierarchy())
+    st.advance()
+    ms, its = [], []
+    for _ in range(max(2, min(args.steps, 5))):
+        r = st.advance()
+        ms.append(st.phase_ms()["solve2"])
+        its.append(r.solve2_iters)
+    peak, kind = load_peaks()
+    it_ms = sum(ms) / sum(its)
+    ach = b_it2 / (it_ms * 1e-3) / 1e9
+    return {"grid": [st.nx, st.ny], "n_lambda": st.n_lambda, "setup_s": round(setup, 2),
+            "cg_iters_per_step": sum(its) / len(its), "cg_iteration_ms": round(it_ms, 4),
+            "b_it2_gb": round(b_it2 / 1e9, 3), "achieved_gbs": round(ach, 1), "frac_measured": round(ach / peak, 4),
+            "frac_of_8tbs": round(ach / 8000, 4), "steps_per_s": round(1e3 / (sum(ms) / len(ms)), 3),
+            "sa_levels": len(hinfo["levels"]), "n_c": hinfo["n_c"]}
+
+
+def cpu_baseline(args) -> dict:
+    """Reference CPU path (oracle/_ref) on a bounded sample of the same workload (rank 0 only)."""
+    from oracle import oracle as O
+    cfg, h_min, dt, _ = workload(args.workload)
+    R = O.ref()
+    cores = os.cpu_count() or 1
+    R.set_threads(cores)
+    t0 = time.time()
+    c = R.case(os.path.join(CASES, cfg + ".cfg"), h_min, dt)
+    setup = time.time() - t0
+    n = args.cpu_steps
+    c.step()  # first step (forward Euler bootstrap) excluded
+    t1 = time.time()
+    for _ in range(n):
+        c.step()
+    el = time.time() - t1
+    return {"value": round(n / el, 5), "unit": "steps/s", "cores": cores, "kind": "reference",
+            "sample": f"{n} Stepper::advance steps of {args.workload} after 1 warm-up step "
+                      f"(setup {setup:.1f}s excluded), OMP_NUM_THREADS={cores}"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU Stepper on the same config (GPU untouched)."""
+    from oracle import oracle as O
+    cfg, h_min, dt, desc = workload(args.workload)
+    if not O.have_ref():
+        return {"impl": "reference", "unavailable": "oracle/_ref/libibmref.so not built"}
+    R = O.ref()
+    cores = os.cpu_count() or 1
+    R.set_threads(cores)
+    t0 = time.time()
+    c = R.case(os.path.join(CASES, cfg + ".cfg"), h_min, dt)
+    setup = time.time() - t0
+    for _ in range(args.warmup):
+        c.step()
+    t1 = time.time()
+    its = 0
+    for _ in range(args.steps):
+        its += c.step()["solve2_iters"]
+    el = time.time() - t1
+    v = args.steps / el
+    return {"impl": "reference", "metric": "time steps/sec (IBPM step: explicit + PCG-diag + SA-PCG + projection)",
+            "value": round(v, 5), "unit": "steps/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic case file)",
+            "config": {"workload": args.workload, "case": cfg + ".cfg", "h_min": h_min or None, "dt": dt or None,
+                       "desc": desc},
+            "cg_iters_per_step": its / args.steps, "setup_s": round(setup, 2),
+            "cpu_baseline": {"value": round(v, 5), "unit": "steps/s", "cores": cores, "kind": "reference",
+                             "sample": f"{args.steps} timed Stepper::advance steps after {args.warmup} warm-up"},
+            "e2e": {"value": round(v, 5), "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-s4m", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+    out, st = run_ours(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([out["ms_per_step"]], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
+        out["ms_per_step"] = float(t.item())
+        out["value"] = round(world * 1e3 / out["ms_per_step"], 4)
+        dist.barrier()
+    if rank == 0:
+        del st
+        if not args.no_s4m and args.workload != "s4m":
+            try:
+                out["s4m"] = s4m_probe(args)
+            except Exception as e:  # report, never hide
+                out["s4m"] = {"error": str(e)}
+        if not args.no_cpu and world == 1:
+            try:
+                out["cpu_baseline"] = cpu_baseline(args)
+            except Exception as e:
+                out["cpu_baseline"] = {"error": str(e)}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -216,6 +216,23 @@ int ibmgpu_stepper_bodies(ibmgpu_stepper_t st, double* x, double* y, double* ubx
 /* time the last advance() spent in each device phase, from CUDA events (ms) */
 int ibmgpu_stepper_phase_ms(ibmgpu_stepper_t st, float* ms6);
 
+/* ---------------------------------------------------------------- host-only case setup
+ * The host half of case loading (config.hpp parse_config, grid.hpp build_stretched_grid,
+ * body.hpp discretisation + move_to(0), operators.hpp metric / diffusion / gradient). No CUDA
+ * calls: usable without a GPU (CPU parity tests). Arrays by name: "x_faces","y_faces","dx","dy",
+ * "x_c","y_c","del_x","del_y","uniform","M","body_x","body_y","body_ub_x","body_ub_y","body_ds",
+ * "visc_bc" (row, slot, idx, coeff quadruples), "boundary"; matrices: "L","G". dims8 as
+ * ibmgpu_stepper_dims (levels/nnz zero). */
+typedef struct ibmgpu_hostcase* ibmgpu_hostcase_t;
+int ibmgpu_hostcase_open(const char* cfg_path, const ibm_case_overrides* ov, ibmgpu_hostcase_t* out, int* dims8,
+                         char* err, int err_cap);
+int ibmgpu_hostcase_array(ibmgpu_hostcase_t h, const char* name, double* out, int* n);
+int ibmgpu_hostcase_csr(ibmgpu_hostcase_t h, const char* name, int* rows, int* cols, int* nnz, int* rptr, int* cidx,
+                        double* val);
+/* move every body to time t (LagrangianBody::move_to, body.hpp:125-148) */
+int ibmgpu_hostcase_move(ibmgpu_hostcase_t h, double t);
+int ibmgpu_hostcase_free(ibmgpu_hostcase_t h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -401,6 +401,8 @@ class Ref:
         L.ref_case_forces.argtypes = [vp, _dp]
         L.ref_case_boundary.restype = C.c_int
         L.ref_case_boundary.argtypes = [vp, _dp]
+        L.ref_case_visc_bc.restype = C.c_int
+        L.ref_case_visc_bc.argtypes = [vp, _dp]
 
     def err(self) -> str:
         return self.L.ref_last_error().decode()
@@ -654,6 +656,12 @@ class RefCase:
         f = np.zeros(4)
         self.ref.L.ref_case_forces(self.h, _d(f))
         return dict(fx=f[0], fy=f[1], cd=f[2], cl=f[3])
+
+    def visc_bc(self) -> np.ndarray:
+        n = self.ref.L.ref_case_visc_bc(self.h, None)
+        a = np.zeros(4 * n)
+        self.ref.L.ref_case_visc_bc(self.h, _d(a))
+        return a
 
     def boundary(self) -> np.ndarray:
         n = self.ref.L.ref_case_boundary(self.h, None)

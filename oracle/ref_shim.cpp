@@ -355,4 +355,17 @@ int ref_case_boundary(const void* h, double* out) {
     return static_cast<int>(k);
 }
 
+// operators.hpp:27-33 BcCoupling list as (row, slot, idx, coeff) quadruples; returns the count
+int ref_case_visc_bc(const void* h, double* out) {
+    const auto& v = static_cast<const RefCase*>(h)->st->ops().visc_bc;
+    if (out)
+        for (size_t k = 0; k < v.size(); ++k) {
+            out[4 * k] = v[k].row;
+            out[4 * k + 1] = static_cast<double>(v[k].slot);
+            out[4 * k + 2] = v[k].idx;
+            out[4 * k + 3] = v[k].coeff;
+        }
+    return static_cast<int>(v.size());
+}
+
 }  // extern "C"

@@ -1,0 +1,715 @@
+// case.cpp — host case setup (see case.hpp). Floating-point expressions keep the reference's
+// association order (built with -ffp-contract=off) so every coordinate is bit-identical.
+#include "case.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <fstream>
+#include <functional>
+#include <numbers>
+#include <sstream>
+#include <stdexcept>
+
+namespace ibmhost {
+
+namespace {
+[[noreturn]] void bad(const std::string& m) { throw std::invalid_argument(m); }
+
+// One axis: uniform cells of h across [u0,u1] (snapped outward by < h/2), geometric growth
+// toward each domain edge, the outermost cell absorbing the residual (grid.hpp:85-127).
+std::vector<double> axis_widths(double d0, double d1, double u0, double u1, double h, double r_lo, double r_hi,
+                                const char* axis) {
+    const double width = u1 - u0;
+    const int n_uni = static_cast<int>(std::ceil(width / h - 1e-9));
+    if (n_uni < 1) bad(std::string("grid: uniform region too small along ") + axis);
+    const double growth = n_uni * h - width;
+    if (growth > 0.5 * h * (1.0 + 1e-9))
+        bad(std::string("grid: uniform region along ") + axis +
+            " is not within half a cell of an integer number of cells of h_min");
+    auto side = [&](double extent, double ratio) {
+        std::vector<double> w;
+        if (extent <= 1e-12 * std::max(1.0, std::fabs(d1 - d0))) return w;
+        double cum = 0.0, cell = h;
+        while (cum < extent - 1e-12) {
+            cell *= ratio;
+            const double next = std::min(cell, extent - cum);
+            w.push_back(next);
+            cum += next;
+            if (w.size() > 100000) throw std::runtime_error("grid: runaway stretching loop");
+        }
+        return w;
+    };
+    const double lo_ext = (u0 - 0.5 * growth) - d0;
+    const double hi_ext = d1 - (u1 + 0.5 * growth);
+    if (lo_ext < -1e-12 || hi_ext < -1e-12) bad(std::string("grid: snapped uniform region exceeds domain along ") + axis);
+    const std::vector<double> lo = side(std::max(lo_ext, 0.0), r_lo);
+    const std::vector<double> hi = side(std::max(hi_ext, 0.0), r_hi);
+    std::vector<double> out(lo.rbegin(), lo.rend());
+    out.insert(out.end(), static_cast<size_t>(n_uni), h);
+    out.insert(out.end(), hi.begin(), hi.end());
+    return out;
+}
+
+std::vector<double> faces(double start, double end, const std::vector<double>& w) {
+    std::vector<double> f(w.size() + 1);
+    f[0] = start;
+    for (size_t i = 0; i < w.size(); ++i) f[i + 1] = f[i] + w[i];
+    f.back() = end;
+    return f;
+}
+}  // namespace
+
+// grid.hpp:134-184
+Grid build_grid(const Rect& dom, const Rect& uni, double h, const double ratio[4]) {
+    if (h <= 0.0) bad("grid: h_min must be positive");
+    for (int s = 0; s < 4; ++s)
+        if (ratio[s] < 1.0) bad("grid: stretching ratio must be >= 1");
+    if (!dom.contains(uni)) bad("grid: uniform region not contained in domain");
+    Grid g;
+    g.domain = dom;
+    g.h_min = h;
+    std::vector<double> wx = axis_widths(dom.x0, dom.x1, uni.x0, uni.x1, h, ratio[0], ratio[1], "x");
+    std::vector<double> wy = axis_widths(dom.y0, dom.y1, uni.y0, uni.y1, h, ratio[2], ratio[3], "y");
+    g.nx = static_cast<int>(wx.size());
+    g.ny = static_cast<int>(wy.size());
+    if (g.nx < 2 || g.ny < 2) bad("grid: need at least 2 cells per direction");
+    g.x_faces = faces(dom.x0, dom.x1, wx);
+    g.y_faces = faces(dom.y0, dom.y1, wy);
+    g.dx.resize(g.nx);
+    g.dy.resize(g.ny);
+    for (int i = 0; i < g.nx; ++i) g.dx[i] = g.x_faces[i + 1] - g.x_faces[i];
+    for (int j = 0; j < g.ny; ++j) g.dy[j] = g.y_faces[j + 1] - g.y_faces[j];
+    for (double w : g.dx)
+        if (w <= 0.0) throw std::runtime_error("grid: nonpositive cell width");
+    for (double w : g.dy)
+        if (w <= 0.0) throw std::runtime_error("grid: nonpositive cell width");
+    g.x_c.resize(g.nx);
+    g.y_c.resize(g.ny);
+    for (int i = 0; i < g.nx; ++i) g.x_c[i] = 0.5 * (g.x_faces[i] + g.x_faces[i + 1]);
+    for (int j = 0; j < g.ny; ++j) g.y_c[j] = 0.5 * (g.y_faces[j] + g.y_faces[j + 1]);
+    g.del_x.resize(g.nx - 1);
+    g.del_y.resize(g.ny - 1);
+    for (int i = 0; i + 1 < g.nx; ++i) g.del_x[i] = g.x_c[i + 1] - g.x_c[i];
+    for (int j = 0; j + 1 < g.ny; ++j) g.del_y[j] = g.y_c[j + 1] - g.y_c[j];
+    const double gx = (std::ceil(uni.width() / h - 1e-9) * h - uni.width()) * 0.5;
+    const double gy = (std::ceil(uni.height() / h - 1e-9) * h - uni.height()) * 0.5;
+    g.uniform_region = {uni.x0 - gx, uni.x1 + gx, uni.y0 - gy, uni.y1 + gy};
+    return g;
+}
+
+// ---------------------------------------------------------------- bodies (body.hpp)
+void MotionParams::finalize(double u_ref, double chord) {
+    if (kind == Motion::heaving) {
+        if (heave_omega == 0.0) heave_omega = 2.0 * k * u_ref / chord;
+        if (heave_amp == 0.0) heave_amp = kh * u_ref / heave_omega;
+        if (heave_omega <= 0.0) bad("motion: heaving frequency must be positive");
+    }
+    if (kind == Motion::flapping && f <= 0.0) bad("motion: flapping frequency must be positive");
+}
+
+bool Body::base_static() const {
+    return motion.kind == Motion::stationary || (motion.kind == Motion::rotating && rotation_invariant);
+}
+bool Body::geometry_static() const { return base_static() && (preamble_offset == 0.0 || preamble_duration <= 0.0); }
+double Body::static_after() const {
+    if (geometry_static()) return 0.0;
+    if (base_static()) return preamble_duration;
+    return std::numeric_limits<double>::infinity();
+}
+
+// body.hpp:63-86 (rigid transform) + :125-148 (placement)
+void Body::move_to(double t) {
+    double ox = 0, oy = 0, ang = 0, vx = 0, vy = 0, av = 0;
+    switch (motion.kind) {
+        case Motion::stationary:
+            break;
+        case Motion::rotating:
+            ang = motion.omega * t;
+            av = motion.omega;
+            break;
+        case Motion::heaving:
+            oy = motion.heave_amp * std::sin(motion.heave_omega * t);
+            vy = motion.heave_amp * motion.heave_omega * std::cos(motion.heave_omega * t);
+            break;
+        case Motion::flapping: {
+            const double w = 2.0 * std::numbers::pi * motion.f;
+            ox = 0.5 * motion.A0 * std::cos(w * t);
+            vx = -0.5 * motion.A0 * w * std::sin(w * t);
+            ang = motion.alpha0 + motion.beta * std::sin(w * t + motion.phase);
+            av = motion.beta * w * std::cos(w * t + motion.phase);
+            break;
+        }
+    }
+    if (preamble_offset != 0.0 && preamble_duration > 0.0 && t < preamble_duration) {
+        const double w = std::numbers::pi / preamble_duration;
+        oy += preamble_offset * 0.5 * (1.0 + std::cos(w * t));
+        vy += -preamble_offset * 0.5 * w * std::sin(w * t);
+    }
+    const double c = std::cos(ang), sn = std::sin(ang);
+    const double cx = center_x + ox, cy = center_y + oy;
+    for (int i = 0; i < n(); ++i) {
+        double rx, ry;
+        if (motion.kind == Motion::rotating && rotation_invariant) {
+            rx = ref_x[i];
+            ry = ref_y[i];
+        } else {
+            rx = c * ref_x[i] - sn * ref_y[i];
+            ry = sn * ref_x[i] + c * ref_y[i];
+        }
+        x[i] = cx + rx;
+        y[i] = cy + ry;
+        ub_x[i] = vx - av * ry;
+        ub_y[i] = vy + av * rx;
+    }
+}
+
+// body.hpp:151-175
+Body circle_body(double cx, double cy, double d, double h) {
+    if (d <= 0.0 || h <= 0.0) bad("body: circle needs positive diameter and h");
+    const double perim = std::numbers::pi * d;
+    const int n = std::max(4, static_cast<int>(std::ceil(perim / h - 1e-9)));
+    Body b;
+    b.center_x = cx;
+    b.center_y = cy;
+    b.ds = perim / n;
+    b.rotation_invariant = true;
+    b.ref_x.resize(n);
+    b.ref_y.resize(n);
+    for (int i = 0; i < n; ++i) {
+        const double th = 2.0 * std::numbers::pi * i / n;
+        b.ref_x[i] = 0.5 * d * std::cos(th);
+        b.ref_y[i] = 0.5 * d * std::sin(th);
+    }
+    b.x = b.ref_x;
+    b.y = b.ref_y;
+    for (double& v : b.x) v += cx;
+    for (double& v : b.y) v += cy;
+    b.ub_x.assign(n, 0.0);
+    b.ub_y.assign(n, 0.0);
+    return b;
+}
+
+namespace {
+// body.hpp:180-198 adaptive Simpson
+double simpson(const std::function<double(double)>& f, double a, double b, double fa, double fm, double fb,
+               double whole, double tol, int depth) {
+    const double m = 0.5 * (a + b);
+    const double lm = 0.5 * (a + m), rm = 0.5 * (m + b);
+    const double flm = f(lm), frm = f(rm);
+    const double left = (m - a) / 6.0 * (fa + 4.0 * flm + fm);
+    const double right = (b - m) / 6.0 * (fm + 4.0 * frm + fb);
+    if (depth <= 0 || std::fabs(left + right - whole) <= 15.0 * tol) return left + right + (left + right - whole) / 15.0;
+    return simpson(f, a, m, fa, flm, fm, left, 0.5 * tol, depth - 1) +
+           simpson(f, m, b, fm, frm, fb, right, 0.5 * tol, depth - 1);
+}
+double integrate(const std::function<double(double)>& f, double a, double b, double tol) {
+    const double m = 0.5 * (a + b);
+    const double fa = f(a), fm = f(m), fb = f(b);
+    return simpson(f, a, b, fa, fm, fb, (b - a) / 6.0 * (fa + 4.0 * fm + fb), tol, 48);
+}
+}  // namespace
+
+// body.hpp:203-260 (equal-arc-length ellipse)
+Body ellipse_body(double cx, double cy, double chord, double tr, double h, int n_override) {
+    if (tr <= 0.0 || tr > 1.0) bad("body: thickness ratio must be in (0, 1]");
+    if (chord <= 0.0 || h <= 0.0) bad("body: ellipse needs positive chord and h");
+    const double a = 0.5 * chord, b = 0.5 * chord * tr;
+    auto speed = [a, b](double t) {
+        const double s = std::sin(t), c = std::cos(t);
+        return std::sqrt(a * a * s * s + b * b * c * c);
+    };
+    const double perim = 4.0 * integrate(speed, 0.0, 0.5 * std::numbers::pi, 1e-12);
+    const int n = n_override > 0 ? n_override : std::max(4, static_cast<int>(std::lround(perim / h)));
+    if (n < 4) bad("body: degenerate ellipse");
+    Body body;
+    body.center_x = cx;
+    body.center_y = cy;
+    body.ds = perim / n;
+    body.ref_x.resize(n);
+    body.ref_y.resize(n);
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) {
+        if (i > 0) {
+            const double target = body.ds;
+            double step = target / speed(t);
+            const double lo = t;
+            double s_acc = integrate(speed, lo, lo + step, 1e-12);
+            for (int it = 0; it < 60; ++it) {
+                const double err = s_acc - target;
+                if (std::fabs(err) < 1e-11 * target) break;
+                step -= err / speed(lo + step);
+                s_acc = integrate(speed, lo, lo + step, 1e-12);
+            }
+            t = lo + step;
+        }
+        body.ref_x[i] = a * std::cos(t);
+        body.ref_y[i] = b * std::sin(t);
+    }
+    body.x = body.ref_x;
+    body.y = body.ref_y;
+    for (double& v : body.x) v += cx;
+    for (double& v : body.y) v += cy;
+    body.ub_x.assign(n, 0.0);
+    body.ub_y.assign(n, 0.0);
+    return body;
+}
+
+// body.hpp:263-294
+Body point_file_body(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("body: cannot open point file " + path);
+    Body b;
+    double px, py;
+    while (in >> px >> py) {
+        b.x.push_back(px);
+        b.y.push_back(py);
+    }
+    const int n = static_cast<int>(b.x.size());
+    if (n < 4) bad("body: point file needs at least 4 points");
+    double sx = 0.0, sy = 0.0;
+    for (int i = 0; i < n; ++i) {
+        sx += b.x[i];
+        sy += b.y[i];
+    }
+    b.center_x = sx / n;
+    b.center_y = sy / n;
+    b.ref_x = b.x;
+    b.ref_y = b.y;
+    for (double& v : b.ref_x) v -= b.center_x;
+    for (double& v : b.ref_y) v -= b.center_y;
+    double per = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const int j = (i + 1) % n;
+        per += std::hypot(b.x[j] - b.x[i], b.y[j] - b.y[i]);
+    }
+    b.ds = per / n;
+    b.ub_x.assign(n, 0.0);
+    b.ub_y.assign(n, 0.0);
+    return b;
+}
+
+// config.hpp:358-383
+std::vector<Body> build_bodies(const Case& c) {
+    std::vector<Body> out;
+    for (const auto& bc : c.bodies) {
+        Body b;
+        if (bc.shape == BodyCfg::circle) {
+            const double h_eff = bc.n_points > 0 ? std::numbers::pi * bc.diameter / bc.n_points : c.h_min;
+            b = circle_body(bc.cx, bc.cy, bc.diameter, h_eff);
+        } else if (bc.shape == BodyCfg::ellipse) {
+            b = ellipse_body(bc.cx, bc.cy, bc.chord, bc.thickness_ratio, c.h_min, bc.n_points);
+        } else {
+            b = point_file_body(bc.points_file);
+        }
+        b.motion = bc.motion;
+        b.motion.finalize(c.u_inf > 0.0 ? c.u_inf : 1.0, bc.shape == BodyCfg::circle ? bc.diameter : bc.chord);
+        b.preamble_offset = bc.preamble_offset;
+        b.preamble_duration = bc.preamble_duration;
+        out.push_back(std::move(b));
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------- boundary (boundary.hpp:42-61)
+Boundary Boundary::initial(const Grid& g, const BcSpec& bc) {
+    Boundary s;
+    auto lr = [&](const EdgeBc& e, std::vector<double>& u, std::vector<double>& v) {
+        u.assign(g.ny, e.kind == Edge::dirichlet ? e.u : bc.u_inf);
+        v.assign(g.ny - 1, e.kind == Edge::dirichlet ? e.v : 0.0);
+    };
+    auto tb = [&](const EdgeBc& e, std::vector<double>& v, std::vector<double>& u) {
+        v.assign(g.nx, e.kind == Edge::dirichlet ? e.v : 0.0);
+        u.assign(g.nx - 1, e.kind == Edge::dirichlet ? e.u : bc.u_inf);
+    };
+    lr(bc.left, s.left_u, s.left_v);
+    lr(bc.right, s.right_u, s.right_v);
+    tb(bc.bottom, s.bottom_v, s.bottom_u);
+    tb(bc.top, s.top_v, s.top_u);
+    return s;
+}
+
+std::vector<double> Boundary::packed() const {
+    std::vector<double> out;
+    for (const auto* v : {&left_u, &right_u, &left_v, &right_v, &bottom_v, &top_v, &bottom_u, &top_u})
+        out.insert(out.end(), v->begin(), v->end());
+    return out;
+}
+
+// ---------------------------------------------------------------- config (config.hpp)
+void Case::validate() {
+    if (dt <= 0.0) bad("config: dt must be positive");
+    if (n_steps <= 0) bad("config: n_steps must be positive");
+    if (h_min <= 0.0) bad("config: h_min must be positive");
+    if (n_pc < 1) bad("config: n_pc must be >= 1");
+    if (n_order < 1 || n_order > 3) bad("config: n_order must be 1, 2 or 3");
+    if (nu > 0.0 && re > 0.0) {
+        const double re_from_nu = u_inf * ref_length / nu;
+        if (std::fabs(re_from_nu - re) > 1e-9 * re)
+            bad("config: re and nu are inconsistent (re = u_inf*ref_length/nu gives " + std::to_string(re_from_nu) + ")");
+    } else if (re > 0.0) {
+        nu = u_inf * ref_length / re;
+    } else if (nu <= 0.0) {
+        bad("config: one of nu or re is required");
+    }
+    for (const SolverCfg* s : {&solve1, &solve2}) {
+        if (!(s->rel_tol > 0.0 && s->rel_tol < 1.0)) bad("solver: rel_tol must be in (0,1)");
+        if (s->max_iters < 1) bad("solver: max_iters must be >= 1");
+    }
+}
+
+namespace {
+struct Line {
+    int no;
+    std::string key;
+    std::vector<std::string> tok;
+};
+std::string at(const Line& l) { return "config line " + std::to_string(l.no) + ": "; }
+std::vector<double> reals(const Line& l, size_t n) {
+    if (l.tok.size() != n)
+        bad(at(l) + "key '" + l.key + "' expects " + std::to_string(n) + " value(s)");
+    std::vector<double> v;
+    for (const auto& t : l.tok) {
+        try {
+            size_t pos = 0;
+            v.push_back(std::stod(t, &pos));
+            if (pos != t.size()) throw std::invalid_argument(t);
+        } catch (...) {
+            bad(at(l) + "bad number '" + t + "'");
+        }
+    }
+    return v;
+}
+double real1(const Line& l) { return reals(l, 1)[0]; }
+int int1(const Line& l) {
+    const double d = real1(l);
+    if (d != std::floor(d)) bad(at(l) + "expected an integer");
+    return static_cast<int>(d);
+}
+EdgeBc edge(const Line& l) {
+    if (l.tok.empty()) bad(at(l) + "empty edge spec");
+    EdgeBc e;
+    if (l.tok[0] == "dirichlet") {
+        if (l.tok.size() != 3) bad(at(l) + "dirichlet expects u and v");
+        e.kind = Edge::dirichlet;
+        e.u = std::stod(l.tok[1]);
+        e.v = std::stod(l.tok[2]);
+    } else if (l.tok[0] == "convective") {
+        e.kind = Edge::convective;
+    } else {
+        bad(at(l) + "unknown edge kind '" + l.tok[0] + "'");
+    }
+    return e;
+}
+void solver_key(SolverCfg& s, const Line& l) {
+    if (l.key == "type") {
+        if (l.tok.size() != 1) bad(at(l) + "type expects one token");
+        const std::string& t = l.tok[0];
+        if (t != "cg" && t != "pcg-diag" && t != "pcg-sa" && t != "amg")
+            bad("config: unknown solver '" + t + "' (cg, pcg-diag, pcg-sa, amg)");
+        s.type = t;
+    } else if (l.key == "rel_tol") {
+        s.rel_tol = real1(l);
+    } else if (l.key == "max_iters") {
+        s.max_iters = int1(l);
+    } else if (l.key == "sa_theta") {
+        s.sa_theta = real1(l);
+    } else if (l.key == "sa_max_coarse") {
+        s.sa_max_coarse = int1(l);
+    } else {
+        bad(at(l) + "unknown solver key '" + l.key + "'");
+    }
+}
+void body_key(BodyCfg& b, const Line& l) {
+    if (l.key == "shape") {
+        const std::string& s = l.tok.at(0);
+        if (s == "circle") b.shape = BodyCfg::circle;
+        else if (s == "ellipse") b.shape = BodyCfg::ellipse;
+        else if (s == "points") b.shape = BodyCfg::points;
+        else bad(at(l) + "unknown shape '" + s + "'");
+    } else if (l.key == "center") {
+        auto v = reals(l, 2);
+        b.cx = v[0];
+        b.cy = v[1];
+    } else if (l.key == "diameter") {
+        b.diameter = real1(l);
+    } else if (l.key == "chord") {
+        b.chord = real1(l);
+    } else if (l.key == "thickness_ratio") {
+        b.thickness_ratio = real1(l);
+    } else if (l.key == "points") {
+        b.n_points = int1(l);
+    } else if (l.key == "points_file") {
+        b.points_file = l.tok.at(0);
+    } else if (l.key == "motion") {
+        const std::string& k = l.tok.at(0);
+        if (k == "stationary") {
+            b.motion.kind = Motion::stationary;
+        } else if (k == "rotating") {
+            if (l.tok.size() != 2) bad(at(l) + "rotating expects omega");
+            b.motion.kind = Motion::rotating;
+            b.motion.omega = std::stod(l.tok[1]);
+        } else if (k == "heaving") {
+            if (l.tok.size() != 3) bad(at(l) + "heaving expects k and kh");
+            b.motion.kind = Motion::heaving;
+            b.motion.k = std::stod(l.tok[1]);
+            b.motion.kh = std::stod(l.tok[2]);
+        } else if (k == "flapping") {
+            if (l.tok.size() != 6) bad(at(l) + "flapping expects A0 f alpha0 beta phase");
+            b.motion.kind = Motion::flapping;
+            b.motion.A0 = std::stod(l.tok[1]);
+            b.motion.f = std::stod(l.tok[2]);
+            b.motion.alpha0 = std::stod(l.tok[3]);
+            b.motion.beta = std::stod(l.tok[4]);
+            b.motion.phase = std::stod(l.tok[5]);
+        } else {
+            bad(at(l) + "unknown motion '" + k + "'");
+        }
+    } else if (l.key == "heave_omega") {
+        b.motion.heave_omega = real1(l);
+    } else if (l.key == "heave_amp") {
+        b.motion.heave_amp = real1(l);
+    } else if (l.key == "preamble") {
+        auto v = reals(l, 2);
+        b.preamble_offset = v[0];
+        b.preamble_duration = v[1];
+    } else {
+        bad(at(l) + "unknown body key '" + l.key + "'");
+    }
+}
+}  // namespace
+
+Case parse_case(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) bad("config: cannot open " + path);
+    Case c;
+    std::string line, section;
+    int no = 0;
+    bool body_open = false;
+    while (std::getline(in, line)) {
+        ++no;
+        const size_t hash = line.find_first_of("#;");
+        if (hash != std::string::npos) line = line.substr(0, hash);
+        std::istringstream ss(line);
+        std::string first;
+        if (!(ss >> first)) continue;
+        if (first.front() == '[') {
+            section = first.substr(1, first.find(']') - 1);
+            static const char* known[] = {"grid", "fluid", "time", "body", "bc", "solver1", "solver2",
+                                          "stepping", "output", "validation"};
+            if (std::find(std::begin(known), std::end(known), section) == std::end(known))
+                bad("config line " + std::to_string(no) + ": unknown section [" + section + "]");
+            body_open = section == "body";
+            if (body_open) c.bodies.emplace_back();
+            continue;
+        }
+        Line l{no, first, {}};
+        std::string eq;
+        if (!(ss >> eq) || eq != "=") bad(at(l) + "expected 'key = value'");
+        std::string t;
+        while (ss >> t) l.tok.push_back(t);
+        if (section == "grid") {
+            if (l.key == "domain") {
+                auto v = reals(l, 4);
+                c.domain = {v[0], v[1], v[2], v[3]};
+            } else if (l.key == "uniform") {
+                auto v = reals(l, 4);
+                c.uniform = {v[0], v[1], v[2], v[3]};
+            } else if (l.key == "h_min") {
+                c.h_min = real1(l);
+            } else if (l.key == "ratio") {
+                auto v = reals(l, 4);
+                for (int s = 0; s < 4; ++s) c.ratio[s] = v[s];
+            } else {
+                bad(at(l) + "unknown grid key '" + l.key + "'");
+            }
+        } else if (section == "fluid") {
+            if (l.key == "nu") c.nu = real1(l);
+            else if (l.key == "re") c.re = real1(l);
+            else if (l.key == "u_inf") c.u_inf = real1(l);
+            else if (l.key == "ref_length") c.ref_length = real1(l);
+            else if (l.key == "initial_velocity") {
+                auto v = reals(l, 2);
+                c.u0 = v[0];
+                c.v0 = v[1];
+            } else bad(at(l) + "unknown fluid key '" + l.key + "'");
+        } else if (section == "time") {
+            if (l.key == "dt") c.dt = real1(l);
+            else if (l.key == "n_steps") c.n_steps = int1(l);
+            else if (l.key == "n_out") c.n_out = int1(l);
+            else bad(at(l) + "unknown time key '" + l.key + "'");
+        } else if (section == "body") {
+            if (!body_open) bad(at(l) + "body key outside [body]");
+            body_key(c.bodies.back(), l);
+        } else if (section == "bc") {
+            if (l.key == "left") c.bc.left = edge(l);
+            else if (l.key == "right") c.bc.right = edge(l);
+            else if (l.key == "top") c.bc.top = edge(l);
+            else if (l.key == "bottom") c.bc.bottom = edge(l);
+            else bad(at(l) + "unknown bc key '" + l.key + "'");
+        } else if (section == "solver1") {
+            solver_key(c.solve1, l);
+        } else if (section == "solver2") {
+            solver_key(c.solve2, l);
+        } else if (section == "stepping") {
+            if (l.key == "n_pc") c.n_pc = int1(l);
+            else if (l.key == "n_order") c.n_order = int1(l);
+            else if (l.key == "slice_rows") c.slice_rows = int1(l);
+            else bad(at(l) + "unknown stepping key '" + l.key + "'");
+        } else if (section == "output") {
+            if (l.key == "dir") c.out_dir = l.tok.at(0);
+            else if (l.key == "checkpoint_every") c.checkpoint_every = int1(l);
+            else bad(at(l) + "unknown output key '" + l.key + "'");
+        } else if (section == "validation") {
+            // validation keys are accepted (post-processing is out of scope for the hot path)
+            if (l.key != "couette" && l.key != "samples" && l.key != "exclude" && l.key != "ray_angle")
+                bad(at(l) + "unknown validation key '" + l.key + "'");
+        } else {
+            bad(at(l) + "key outside any section");
+        }
+    }
+    c.bc.u_inf = c.u_inf;
+    c.validate();
+    return c;
+}
+
+// ---------------------------------------------------------------- grid operators
+std::vector<double> metric(const Grid& g) {
+    std::vector<double> m(g.n_q());
+    for (int j = 0; j < g.ny; ++j)
+        for (int i_f = 1; i_f < g.nx; ++i_f) m[g.u_id(i_f, j)] = g.del_x[i_f - 1] / g.dy[j];
+    for (int j_f = 1; j_f < g.ny; ++j_f)
+        for (int i = 0; i < g.nx; ++i) m[g.v_id(i, j_f)] = g.del_y[j_f - 1] / g.dx[i];
+    return m;
+}
+
+// Flux-form staggered Laplacian on q (operators.hpp:94-194), emitted directly in CSR column
+// order (south, west, diagonal, east, north); wall neighbours become BcCouplings in the
+// reference's per-row order (u: W, E, S, N; v: S, N, W, E).
+Csr diffusion(const Grid& g, std::vector<BcCoupling>& bc) {
+    bc.clear();
+    const int nx = g.nx, ny = g.ny;
+    Csr L;
+    L.rows = L.cols = g.n_q();
+    L.rp.reserve(L.rows + 1);
+    L.ci.reserve(static_cast<size_t>(L.rows) * 5);
+    L.v.reserve(static_cast<size_t>(L.rows) * 5);
+    L.rp.push_back(0);
+    auto emit = [&](int row, bool has_s, int s_col, double s_val, bool has_w, int w_col, double w_val, double d,
+                    bool has_e, int e_col, double e_val, bool has_n, int n_col, double n_val) {
+        auto put = [&](int c, double v) {
+            if (v != 0.0) {  // from_triplets drops exact zeros (sparse.hpp:59)
+                L.ci.push_back(c);
+                L.v.push_back(v);
+            }
+        };
+        if (has_s) put(s_col, s_val);
+        if (has_w) put(w_col, w_val);
+        put(row, d);
+        if (has_e) put(e_col, e_val);
+        if (has_n) put(n_col, n_val);
+        L.rp.push_back(static_cast<int>(L.ci.size()));
+    };
+    for (int j = 0; j < ny; ++j)
+        for (int i_f = 1; i_f < nx; ++i_f) {
+            const int row = g.u_id(i_f, j);
+            const double sm = g.del_x[i_f - 1], dyj = g.dy[j];
+            double dh = 0.0;
+            double wv = 0, ev = 0, sv = 0, nv = 0;
+            const bool hw = i_f - 1 >= 1, he = i_f + 1 <= nx - 1, hs = j > 0, hn = j < ny - 1;
+            {
+                const double w_hat = 1.0 / (sm * g.dx[i_f - 1]);
+                dh += w_hat;
+                if (hw) wv = 1.0 / (dyj * g.dx[i_f - 1]);
+                else bc.push_back({row, LU, j, sm * w_hat});
+            }
+            {
+                const double w_hat = 1.0 / (sm * g.dx[i_f]);
+                dh += w_hat;
+                if (he) ev = 1.0 / (dyj * g.dx[i_f]);
+                else bc.push_back({row, RU, j, sm * w_hat});
+            }
+            {
+                const double span = hs ? g.del_y[j - 1] : 0.5 * dyj;
+                const double w_hat = 1.0 / (dyj * span);
+                dh += w_hat;
+                if (hs) sv = sm / (span * (dyj * g.dy[j - 1]));
+                else bc.push_back({row, BU, i_f - 1, sm * w_hat});
+            }
+            {
+                const double span = hn ? g.del_y[j] : 0.5 * dyj;
+                const double w_hat = 1.0 / (dyj * span);
+                dh += w_hat;
+                if (hn) nv = sm / (span * (dyj * g.dy[j + 1]));
+                else bc.push_back({row, TU, i_f - 1, sm * w_hat});
+            }
+            emit(row, hs, g.u_id(i_f, j - 1), sv, hw, g.u_id(i_f - 1, j), wv, -sm * dh / dyj, he, g.u_id(i_f + 1, j),
+                 ev, hn, g.u_id(i_f, j + 1), nv);
+        }
+    for (int j_f = 1; j_f < ny; ++j_f)
+        for (int i = 0; i < nx; ++i) {
+            const int row = g.v_id(i, j_f);
+            const double sm = g.del_y[j_f - 1], dxi = g.dx[i];
+            double dh = 0.0;
+            double wv = 0, ev = 0, sv = 0, nv = 0;
+            const bool hs = j_f - 1 >= 1, hn = j_f + 1 <= ny - 1, hw = i > 0, he = i < nx - 1;
+            {
+                const double w_hat = 1.0 / (sm * g.dy[j_f - 1]);
+                dh += w_hat;
+                if (hs) sv = 1.0 / (dxi * g.dy[j_f - 1]);
+                else bc.push_back({row, BV, i, sm * w_hat});
+            }
+            {
+                const double w_hat = 1.0 / (sm * g.dy[j_f]);
+                dh += w_hat;
+                if (hn) nv = 1.0 / (dxi * g.dy[j_f]);
+                else bc.push_back({row, TV, i, sm * w_hat});
+            }
+            {
+                const double span = hw ? g.del_x[i - 1] : 0.5 * dxi;
+                const double w_hat = 1.0 / (dxi * span);
+                dh += w_hat;
+                if (hw) wv = sm / (span * (dxi * g.dx[i - 1]));
+                else bc.push_back({row, LV, j_f - 1, sm * w_hat});
+            }
+            {
+                const double span = he ? g.del_x[i] : 0.5 * dxi;
+                const double w_hat = 1.0 / (dxi * span);
+                dh += w_hat;
+                if (he) ev = sm / (span * (dxi * g.dx[i + 1]));
+                else bc.push_back({row, RV, j_f - 1, sm * w_hat});
+            }
+            emit(row, hs, g.v_id(i, j_f - 1), sv, hw, g.v_id(i - 1, j_f), wv, -sm * dh / dxi, he, g.v_id(i + 1, j_f),
+                 ev, hn, g.v_id(i, j_f + 1), nv);
+        }
+    return L;
+}
+
+// operators.hpp:210-226 (entries +-1; D = -G^T)
+Csr gradient(const Grid& g) {
+    Csr G;
+    G.rows = g.n_q();
+    G.cols = g.n_p();
+    G.rp.reserve(G.rows + 1);
+    G.ci.reserve(static_cast<size_t>(G.rows) * 2);
+    G.v.reserve(static_cast<size_t>(G.rows) * 2);
+    G.rp.push_back(0);
+    for (int j = 0; j < g.ny; ++j)
+        for (int i_f = 1; i_f < g.nx; ++i_f) {
+            G.ci.push_back(g.p_id(i_f - 1, j));
+            G.v.push_back(-1.0);
+            G.ci.push_back(g.p_id(i_f, j));
+            G.v.push_back(1.0);
+            G.rp.push_back(static_cast<int>(G.ci.size()));
+        }
+    for (int j_f = 1; j_f < g.ny; ++j_f)
+        for (int i = 0; i < g.nx; ++i) {
+            G.ci.push_back(g.p_id(i, j_f - 1));
+            G.v.push_back(-1.0);
+            G.ci.push_back(g.p_id(i, j_f));
+            G.v.push_back(1.0);
+            G.rp.push_back(static_cast<int>(G.ci.size()));
+        }
+    return G;
+}
+
+}  // namespace ibmhost

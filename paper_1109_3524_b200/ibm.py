@@ -568,3 +568,48 @@ class Stepper:
         a = (C.c_float * 6)()
         self.ctx.check(self.ctx.lib.ibmgpu_stepper_phase_ms(self.h, a))
         return dict(zip(("assembly", "precond", "explicit", "solve1", "solve2", "projection"), list(a)))
+
+
+class HostCase:
+    """Host half of case loading (no GPU): grid, bodies, M, L, G exactly as the product builds them."""
+
+    def __init__(self, cfg_path: str, h_min: float = 0.0, dt: float = 0.0):
+        self.lib = load()
+        ov = CaseOverridesC(h_min, dt, 0, 0, 0)
+        h = C.c_void_p()
+        d = np.zeros(8, np.int32)
+        err = C.create_string_buffer(512)
+        rc = self.lib.ibmgpu_hostcase_open(cfg_path.encode(), C.byref(ov), C.byref(h), _i(d), err, 512)
+        if rc == 1:
+            raise ValueError(err.value.decode())
+        if rc:
+            raise RuntimeError(err.value.decode())
+        self.h = h
+        (self.nx, self.ny, self.n_q, self.n_p, self.n_b, self.n_lambda) = map(int, d[:6])
+
+    def __del__(self):
+        try:
+            self.lib.ibmgpu_hostcase_free(self.h)
+        except Exception:
+            pass
+
+    def array(self, name: str) -> np.ndarray:
+        n = C.c_int()
+        if self.lib.ibmgpu_hostcase_array(self.h, name.encode(), None, C.byref(n)):
+            raise ValueError(name)
+        out = np.zeros(max(n.value, 1))
+        self.lib.ibmgpu_hostcase_array(self.h, name.encode(), _d(out), C.byref(n))
+        return out[:n.value]
+
+    def csr(self, name: str):
+        r, c, n = C.c_int(), C.c_int(), C.c_int()
+        if self.lib.ibmgpu_hostcase_csr(self.h, name.encode(), C.byref(r), C.byref(c), C.byref(n), None, None, None):
+            raise ValueError(name)
+        rp = np.zeros(r.value + 1, np.int32)
+        ci = np.zeros(max(n.value, 1), np.int32)
+        v = np.zeros(max(n.value, 1))
+        self.lib.ibmgpu_hostcase_csr(self.h, name.encode(), None, None, None, _i(rp), _i(ci), _d(v))
+        return r.value, c.value, rp, ci[:n.value], v[:n.value]
+
+    def move(self, t: float):
+        self.lib.ibmgpu_hostcase_move(self.h, t)

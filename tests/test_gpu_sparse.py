@@ -21,10 +21,16 @@ def mats():
 
 
 def test_spmv_bitwise(port):
+    """Short-row matrices (SELL-32, thread per row, column-order non-FMA sums) are bit-exact with
+    spmv_into; long-row Galerkin levels use the CSR-vector kernel (lane-strided sums): 1e-14."""
     for m in mats():
         x = np.sin(np.arange(m.cols) * 0.37 + 0.1)
         y = dev(m).spmv(x)
-        assert np.array_equal(y, port.spmv(m, x))
+        yo = port.spmv(m, x)
+        if m.nnz <= 12 * m.rows:
+            assert np.array_equal(y, yo)
+        else:
+            assert np.max(np.abs(y - yo)) <= 1e-14 * np.max(np.abs(m.v)) * np.sum(np.abs(x))
 
 
 def test_spmv_known_answers():
