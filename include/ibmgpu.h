@@ -199,7 +199,8 @@ int ibmgpu_stepper_dims(ibmgpu_stepper_t st, int* dims8);
 int ibmgpu_stepper_scalars(ibmgpu_stepper_t st, double* s6);
 /* Stepper::advance (stepper.hpp:231-356) */
 int ibmgpu_stepper_advance(ibmgpu_stepper_t st, ibm_step_report* rep);
-/* state download: which 0 q, 1 lambda, 2 conv_prev, 3 boundary arrays (BoundaryState order);
+/* state download: which 0 q, 1 lambda, 2 conv_prev, 3 boundary arrays (BoundaryState order),
+ * 4 scalars {t, step_index, have_conv_prev}, 5 f~ (the 2 n_b force entries of lambda);
  * returns the length in *n (pass out=NULL to query). */
 int ibmgpu_stepper_get(ibmgpu_stepper_t st, int which, double* out, int* n);
 /* state upload (checkpoint restore, io.hpp:112-145): same `which` codes */

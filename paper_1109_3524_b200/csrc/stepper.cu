@@ -910,6 +910,7 @@ int ibmgpu_stepper_get(ibmgpu_stepper_t S, int which, double* out, int* n) {
             case 1: src = S->lambda.p, len = S->n_lambda; break;
             case 2: src = S->conv_prev.p, len = S->n_q; break;
             case 3: src = S->bnd.p, len = S->bl.total; break;
+            case 5: src = S->lambda.p + S->n_p, len = 2 * S->n_b; break;
             case 4:
                 scal[0] = S->t, scal[1] = S->step, scal[2] = S->have_conv ? 1.0 : 0.0;
                 len = 3;

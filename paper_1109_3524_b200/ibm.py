@@ -488,7 +488,7 @@ class StepReport:
 class Stepper:
     """Device-resident Stepper (stepper.hpp:169-370) over a case file (config.hpp format)."""
 
-    STATE = {"q": 0, "lambda": 1, "conv_prev": 2, "boundary": 3}
+    STATE = {"q": 0, "lambda": 1, "conv_prev": 2, "boundary": 3, "scalars": 4, "f_tilde": 5}
     GRID = ("x_faces", "y_faces", "dx", "dy", "x_c", "y_c", "del_x", "del_y")
 
     def __init__(self, cfg_path: str, h_min: float = 0.0, dt: float = 0.0, n_pc: int = 0,

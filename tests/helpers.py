@@ -77,3 +77,9 @@ def assert_csr_equal(a: O.Csr, b: O.Csr, values: str = "bitwise", rtol: float = 
     else:
         scale = max(np.max(np.abs(b.v)) if b.nnz else 0.0, 1e-300)
         assert np.max(np.abs(a.v - b.v)) <= rtol * scale if a.nnz else True
+
+
+def rel_err(a, b):
+    a = np.asarray(a, float)
+    b = np.asarray(b, float)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)) if a.size else 0.0
