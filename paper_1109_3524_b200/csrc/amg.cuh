@@ -71,6 +71,10 @@ struct EpiJacobiResidual {  // K1: x_i = wd_i b_i ; r_i = b_i - s
     double* r;
     const int* done;
     __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ void touch(int i) const {
+        pf(wd + i);
+        pf(b + i);
+    }
     __device__ void row(int i, double s, double*) const {
         const double bi = b[i];
         x[i] = mul(wd[i], bi);
@@ -95,6 +99,7 @@ struct EpiAddInPlace {  // K3: x_i += s
     double* x;
     const int* done;
     __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ void touch(int i) const { pf(x + i); }
     __device__ void row(int i, double s, double*) const { x[i] = addd(x[i], s); }
     __device__ RedSlot slot() const { return {}; }
     __device__ void fin(double*) const {}
@@ -108,6 +113,10 @@ struct EpiPostSmooth {  // K4: out_i = x_i + wd_i (b_i - s)
     double* out;
     const int* done;
     __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ void touch(int i) const {
+        pf(wd + i);
+        pf(b + i);
+    }
     __device__ void row(int i, double s, double*) const { out[i] = addd(x[i], mul(wd[i], subd(b[i], s))); }
     __device__ RedSlot slot() const { return {}; }
     __device__ void fin(double*) const {}
@@ -125,6 +134,10 @@ struct EpiPostSmoothDot {
     RedSlot rs;
     Fin f;
     __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ void touch(int i) const {
+        pf(wd + i);
+        pf(b + i);
+    }
     __device__ void row(int i, double s, double* acc) const {
         const double bi = b[i];
         const double z = addd(x[i], mul(wd[i], subd(bi, s)));

@@ -54,6 +54,8 @@ int ibmgpu_init(int device, int nranks, int rank, const void* nccl_id, ibmgpu_ct
         CK(cudaEventCreate(&c->t0));
         CK(cudaEventCreate(&c->t1));
         CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+        const char* eg = std::getenv("IBMGPU_EAGER");
+        c->eager = eg && eg[0] == '1';
         cudaMemPool_t pool;
         CK(cudaDeviceGetDefaultMemPool(&pool, device));
         unsigned long long thr = ~0ull;  // keep freed blocks cached in the pool

@@ -10,6 +10,8 @@
 // CSR-vector kernel with 4..32 threads per row.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include "internal.cuh"
 #include "kern.cuh"
 
@@ -65,15 +67,16 @@ __global__ void k_slice_width(int rows, const int* __restrict__ rp, int* __restr
 }
 
 __global__ void k_sell_fill(int rows, const int* __restrict__ rp, const int* __restrict__ ci,
-                            const double* __restrict__ v, const int* __restrict__ off, int* __restrict__ sci,
-                            double* __restrict__ sv) {
+                            const double* __restrict__ v, const int* __restrict__ off, const int* __restrict__ perm,
+                            int* __restrict__ sci, double* __restrict__ sv) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int n_slices = (rows + 31) >> 5;
     if (i >= n_slices * 32) return;
     const int s = i >> 5, lane = i & 31;
     const int width = (off[s + 1] - off[s]) >> 5;
-    const int b = i < rows ? rp[i] : 0;
-    const int len = i < rows ? rp[i + 1] - b : 0;
+    const int row = i < rows ? (perm ? perm[i] : i) : -1;
+    const int b = row >= 0 ? rp[row] : 0;
+    const int len = row >= 0 ? rp[row + 1] - b : 0;
     for (int k = 0; k < width; ++k) {
         const int dst = off[s] + 32 * k + lane;
         if (k < len) {
@@ -122,7 +125,7 @@ void mat_plan(Ctx* c, Mat* m) {
     CK_LAUNCH(c);
     m->max_row = d2h_scalar(c, mx.p);
     const double avg = m->rows ? double(m->nnz) / m->rows : 0.0;
-    if (avg <= 12.0) {
+    if (avg <= 12.0 && m->max_row <= 48) {
         m->kind = SPMV_SELL;
         m->sell_off.alloc(c, (size_t)n_slices + 1);
         exclusive_scan_total(c, width.p, m->sell_off.p, n_slices);
@@ -130,11 +133,93 @@ void mat_plan(Ctx* c, Mat* m) {
         m->sell_ci.alloc(c, (size_t)total);
         m->sell_v.alloc(c, (size_t)total);
         k_sell_fill<<<(n_slices * 32 + 255) / 256, 256, 0, c->stream>>>(m->rows, m->rp.p, m->ci.p, m->v.p,
-                                                                        m->sell_off.p, m->sell_ci.p, m->sell_v.p);
+                                                                        m->sell_off.p, nullptr, m->sell_ci.p,
+                                                                        m->sell_v.p);
         CK_LAUNCH(c);
-    } else {
+        return;
+    }
+    std::vector<int> rp(static_cast<size_t>(m->rows) + 1);
+    d2h(c, rp.data(), m->rp.p, rp.size());
+    sync(c);
+    if (m->max_row <= 96) {
+        // SELL-32-sigma: sort rows by length within 512-row windows; accept if padding <= 25%
+        constexpr int kSigma = 512;
+        std::vector<int> perm(static_cast<size_t>(m->rows));
+        for (int w0 = 0; w0 < m->rows; w0 += kSigma) {
+            const int w1 = std::min(m->rows, w0 + kSigma);
+            for (int i = w0; i < w1; ++i) perm[i] = i;
+            std::stable_sort(perm.begin() + w0, perm.begin() + w1,
+                             [&](int a, int b) { return rp[a + 1] - rp[a] > rp[b + 1] - rp[b]; });
+        }
+        std::vector<int> off(static_cast<size_t>(n_slices) + 1, 0);
+        long long total = 0;
+        for (int s = 0; s < n_slices; ++s) {
+            int w = 0;
+            for (int i = s * 32; i < std::min(m->rows, s * 32 + 32); ++i) w = std::max(w, rp[perm[i] + 1] - rp[perm[i]]);
+            total += 32ll * w;
+            off[s + 1] = static_cast<int>(total);
+        }
+        if (total <= (long long)(1.25 * m->nnz) + 32 * 64 && total < (1ll << 31)) {
+            m->kind = SPMV_SELLW;
+            m->perm.alloc(c, perm.size());
+            h2d(c, m->perm.p, perm.data(), perm.size());
+            m->sell_off.alloc(c, off.size());
+            h2d(c, m->sell_off.p, off.data(), off.size());
+            m->sell_ci.alloc(c, (size_t)total);
+            m->sell_v.alloc(c, (size_t)total);
+            k_sell_fill<<<(n_slices * 32 + 255) / 256, 256, 0, c->stream>>>(m->rows, m->rp.p, m->ci.p, m->v.p,
+                                                                            m->sell_off.p, m->perm.p, m->sell_ci.p,
+                                                                            m->sell_v.p);
+            CK_LAUNCH(c);
+            sync(c);
+            return;
+        }
+    }
+    {
+        // CSR-adaptive chunks (kern.cuh k_spmv_adapt), planned on the host from row_ptr
         m->kind = SPMV_VECTOR;
-        m->tpr = avg <= 24.0 ? 4 : avg <= 64.0 ? 8 : avg <= 160.0 ? 16 : 32;
+        constexpr int kChunkNnz = 2048;
+        // rows much longer than the mean never share a CTA with short rows
+        const int kOwnCta = std::max(128, static_cast<int>(4.0 * avg));
+        std::vector<int4> meta;
+        std::vector<int2> lrow;
+        int parts = 0;
+        int r = 0;
+        while (r < m->rows) {
+            const int len = rp[r + 1] - rp[r];
+            if (len > kOwnCta) {  // long row: one CTA per kRowChunk entries (at least one)
+                const int nch = (len + kRowChunk - 1) / kRowChunk;
+                const int lid = static_cast<int>(lrow.size());
+                lrow.push_back(make_int2(parts, nch));
+                for (int q = 0; q < nch; ++q) meta.push_back(make_int4(r, q, 0, lid));
+                parts += nch;
+                ++r;
+                continue;
+            }
+            int r1 = r, nz = 0;
+            while (r1 < m->rows) {
+                const int l = rp[r1 + 1] - rp[r1];
+                if (l > kOwnCta || (r1 > r && (nz + l > kChunkNnz || r1 - r >= 256))) break;
+                nz += l;
+                ++r1;
+            }
+            const double mean = double(nz) / (r1 - r);
+            int tpr = 2;
+            while (tpr < 32 && tpr * 4 < mean) tpr *= 2;
+            // keep at least a few rows per group for short-row chunks
+            while (tpr > 2 && (r1 - r) > (kBlock / tpr) * 8) tpr /= 2;
+            meta.push_back(make_int4(r, r1, tpr, 0));
+            r = r1;
+        }
+        m->n_blocks = static_cast<int>(meta.size());
+        m->blk_meta.alloc(c, meta.size());
+        h2d(c, m->blk_meta.p, meta.data(), meta.size());
+        m->lrow.alloc(c, std::max<size_t>(lrow.size(), 1));
+        h2d(c, m->lrow.p, lrow.data(), lrow.size());
+        m->lpart.alloc(c, (size_t)std::max(parts, 1));
+        m->lcnt.alloc(c, std::max<size_t>(lrow.size(), 1));
+        CK(cudaMemsetAsync(m->lcnt.p, 0, sizeof(unsigned) * std::max<size_t>(lrow.size(), 1), c->stream));
+        sync(c);
     }
 }
 

@@ -49,6 +49,7 @@ struct ibmgpu_ctx {
     int num_sms = 148;
     void* nccl = nullptr;       // ncclComm_t when nranks > 1
     void* pcg_cache = nullptr;  // pcg.cu plan cache
+    int eager = 0;              // IBMGPU_EAGER=1: host-looped solves (profiling only)
 };
 
 namespace ibmgpu {
@@ -113,7 +114,7 @@ inline T d2h_scalar(Ctx* c, const T* src) {
 }
 
 // SpMV execution plan chosen at construction from the row-length profile.
-enum SpmvKind { SPMV_SELL = 0, SPMV_VECTOR = 1 };
+enum SpmvKind { SPMV_SELL = 0, SPMV_VECTOR = 1, SPMV_SELLW = 2 };
 
 }  // namespace ibmgpu
 
@@ -130,6 +131,12 @@ struct ibmgpu_mat {
     ibmgpu::DBuf<int> sell_off;  // n_slices + 1 element offsets
     ibmgpu::DBuf<int> sell_ci;
     ibmgpu::DBuf<double> sell_v;
+    ibmgpu::DBuf<int> perm;              // SELL-sigma: slot -> original row
+    int n_blocks = 0;                   // CSR-adaptive plan (kern.cuh k_spmv_adapt)
+    ibmgpu::DBuf<int4> blk_meta;         // per CTA: {r0, r1, tpr, 0} | {row, chunk, 0, long-row id}
+    ibmgpu::DBuf<int2> lrow;             // per long row: {partial base, chunks}
+    ibmgpu::DBuf<double> lpart;          // long-row chunk partials
+    ibmgpu::DBuf<unsigned> lcnt;         // long-row arrival counters
     bool planned = false;
     bool borrowed = false;  // owned by a hierarchy / stepper; ibmgpu_csr_destroy refuses
 };

@@ -21,6 +21,10 @@ __device__ __forceinline__ double subd(double a, double b) { return __dsub_rn(a,
 constexpr int kBlock = 256;
 constexpr unsigned kFull = 0xffffffffu;
 
+// L1 prefetch of an epilogue operand, issued before the row loop so its DRAM latency overlaps
+// the matrix stream (epilogues opt in by defining touch(i)).
+__device__ __forceinline__ void pf(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
 // ---------------------------------------------------------------- reductions
 template <int NR>
 struct Vals {
@@ -110,66 +114,215 @@ struct XJacobi {
 // Epi::NR > 0 enables a fused grid reduction: epi.row adds into acc[0..NR), and epi.fin(tot)
 // runs once in the last block.
 
+// SELL-32, thread per row, kSellRows rows per thread: every load of both rows (slice entries,
+// epilogue operands) is issued before the first use, doubling the bytes in flight per thread —
+// the level-0 kernels are latency-bound otherwise (ncu: 33% DRAM, long-scoreboard stalls).
+constexpr int kSellRows = 1;
+constexpr int kSellU = 5;  // entries per row loaded up front (5-point rows); wider rows loop
+
 template <class XF, class Epi>
-__global__ void __launch_bounds__(kBlock) k_spmv_sell(int rows, const int* __restrict__ rp,
-                                                      const int* __restrict__ off, const int* __restrict__ ci,
-                                                      const double* __restrict__ v, XF xf, Epi epi) {
+__global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __restrict__ rp,
+                                                         const int* __restrict__ off, const int* __restrict__ ci,
+                                                         const double* __restrict__ v, XF xf, Epi epi) {
     constexpr int NR = Epi::NR;
     if (epi.skip()) return;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
-    const int i = blockIdx.x * kBlock + threadIdx.x;
-    if (i < rows) {
-        const int len = __ldg(rp + i + 1) - __ldg(rp + i);
-        const int base = __ldg(off + (i >> 5)) + (i & 31);
-        double s = 0.0;
-        for (int k0 = 0; k0 < len; k0 += 8) {
-            int c[8];
-            double a[8];
+    const int n_slices = (rows + 31) >> 5;
+    int ix[kSellRows], base[kSellRows], width[kSellRows], len[kSellRows];
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (k0 + u < len) {
-                    c[u] = __ldg(ci + base + 32 * (k0 + u));
-                    a[u] = __ldg(v + base + 32 * (k0 + u));
-                }
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (k0 + u < len) s = addd(s, mul(a[u], xf(c[u])));
+    for (int q = 0; q < kSellRows; ++q) {
+        const int i = (blockIdx.x * kSellRows + q) * kBlock + threadIdx.x;
+        const int sl = i >> 5;
+        // slice loads depend only on the (warp-broadcast) slice offset; the row length only
+        // masks the accumulation, so neither waits on row_ptr
+        const int beg = sl < n_slices ? __ldg(off + sl) : 0;
+        width[q] = sl < n_slices ? (__ldg(off + sl + 1) - beg) >> 5 : 0;
+        base[q] = beg + (i & 31);
+        len[q] = i < rows ? __ldg(rp + i + 1) - __ldg(rp + i) : 0;
+        ix[q] = i;
+        if constexpr (requires { epi.touch(0); }) {
+            if (i < rows) epi.touch(i);
         }
-        epi.row(i, s, acc);
     }
+    int c[kSellRows][kSellU];
+    double a[kSellRows][kSellU];
+#pragma unroll
+    for (int q = 0; q < kSellRows; ++q)
+#pragma unroll
+        for (int u = 0; u < kSellU; ++u)
+            if (u < width[q]) {
+                c[q][u] = __ldg(ci + base[q] + 32 * u);
+                a[q][u] = __ldg(v + base[q] + 32 * u);
+            }
+    double s[kSellRows];
+#pragma unroll
+    for (int q = 0; q < kSellRows; ++q) {
+        s[q] = 0.0;
+#pragma unroll
+        for (int u = 0; u < kSellU; ++u)
+            if (u < len[q]) s[q] = addd(s[q], mul(a[q][u], xf(c[q][u])));
+        for (int k = kSellU; k < len[q]; ++k)  // rows wider than kSellU (body-coupled rows)
+            s[q] = addd(s[q], mul(__ldg(v + base[q] + 32 * k), xf(__ldg(ci + base[q] + 32 * k))));
+    }
+#pragma unroll
+    for (int q = 0; q < kSellRows; ++q)
+        if (ix[q] < rows) epi.row(ix[q], s[q], acc);
     if constexpr (NR > 0) {
         if (grid_sum_last<NR>(acc, epi.slot())) epi.fin(acc);
     }
 }
 
-template <int TPR, class XF, class Epi>
-__global__ void __launch_bounds__(kBlock) k_spmv_vec(int rows, const int* __restrict__ rp,
-                                                     const int* __restrict__ ci, const double* __restrict__ v,
-                                                     XF xf, Epi epi) {
+// SELL-32-sigma for the wider Galerkin levels (15-60 entries per row): rows are sorted by length
+// (descending) within 512-row windows so a slice's rows have similar lengths, slot i holds
+// original row perm[i]. Entries keep their column order, so the sum is still bit-exact with
+// spmv_into. The entry loop is software-pipelined: chunk k+1's indices/values are in flight while
+// chunk k's x-gathers are consumed.
+template <class XF, class Epi>
+__global__ void __launch_bounds__(kBlock, 4) k_spmv_sellw(int rows, const int* __restrict__ rp,
+                                                          const int* __restrict__ perm, const int* __restrict__ off,
+                                                          const int* __restrict__ ci, const double* __restrict__ v,
+                                                          XF xf, Epi epi) {
+    constexpr int NR = Epi::NR;
+    constexpr int U = 4;
+    if (epi.skip()) return;
+    double acc[NR > 0 ? NR : 1];
+#pragma unroll
+    for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    const int sl = i >> 5;
+    const bool in_slice = sl < ((rows + 31) >> 5);
+    const int beg = in_slice ? __ldg(off + sl) : 0;
+    const int width = in_slice ? (__ldg(off + sl + 1) - beg) >> 5 : 0;
+    const int base = beg + (i & 31);
+    const int row = i < rows ? __ldg(perm + i) : -1;
+    const int len = row >= 0 ? __ldg(rp + row + 1) - __ldg(rp + row) : 0;
+    if constexpr (requires { epi.touch(0); }) {
+        if (row >= 0) epi.touch(row);
+    }
+    int c0[U];
+    double a0[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+        if (u < width) {
+            c0[u] = __ldg(ci + base + 32 * u);
+            a0[u] = __ldg(v + base + 32 * u);
+        }
+    double s = 0.0;
+    for (int k0 = 0; k0 < width; k0 += U) {
+        int c1[U];
+        double a1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (k0 + U + u < width) {
+                c1[u] = __ldg(ci + base + 32 * (k0 + U + u));
+                a1[u] = __ldg(v + base + 32 * (k0 + U + u));
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (k0 + u < len) s = addd(s, mul(a0[u], xf(c0[u])));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            c0[u] = c1[u];
+            a0[u] = a1[u];
+        }
+    }
+    if (row >= 0) epi.row(row, s, acc);
+    if constexpr (NR > 0) {
+        if (grid_sum_last<NR>(acc, epi.slot())) epi.fin(acc);
+    }
+}
+
+// CSR-adaptive SpMV for irregular / long-row matrices (Galerkin coarse levels: a few aggregate
+// rows couple to thousands of body rows). The plan cuts the rows into per-CTA chunks of ~2k
+// nonzeros: a chunk is either one long row reduced by the whole CTA, or a run of rows handled by
+// `tpr`-thread groups (tpr in 2..32, chosen from the chunk's mean row length). Every reduction
+// has a fixed order, so results are deterministic.
+// Long rows (> kLongRow entries) are cut into kRowChunk-entry chunks, one CTA each; the last CTA of
+// a row to finish (arrival counter) sums the chunk partials in chunk order and runs the epilogue.
+constexpr int kLongRow = 1024, kRowChunk = 2048;
+
+struct AdaptPlan {
+    const int4* meta;        // {r0, r1, tpr, 0} or, for a long-row chunk, {row, chunk, 0, long-row id}
+    const int2* lrow;        // per long row: {partial base, chunk count}
+    double* lpart;           // chunk partials
+    unsigned* lcnt;          // per long row arrival counters (self-resetting)
+};
+
+template <class XF, class Epi>
+__global__ void __launch_bounds__(kBlock) k_spmv_adapt(AdaptPlan pl, const int* __restrict__ rp,
+                                                       const int* __restrict__ ci, const double* __restrict__ v,
+                                                       XF xf, Epi epi) {
     constexpr int NR = Epi::NR;
     if (epi.skip()) return;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
-    const int g = blockIdx.x * kBlock + threadIdx.x;
-    const int i = g / TPR, lane = g % TPR;
-    double s = 0.0;
-    if (i < rows) {
-        const int e = __ldg(rp + i + 1);
-        int k = __ldg(rp + i) + lane;
-        for (; k + TPR < e; k += 2 * TPR) {
-            const int c0 = __ldg(ci + k), c1 = __ldg(ci + k + TPR);
-            const double a0 = __ldg(v + k), a1 = __ldg(v + k + TPR);
-            s = addd(s, mul(a0, xf(c0)));
-            s = addd(s, mul(a1, xf(c1)));
-        }
-        if (k < e) s = addd(s, mul(__ldg(v + k), xf(__ldg(ci + k))));
-    }
+    const int4 m = __ldg(pl.meta + blockIdx.x);
+    const int tpr = m.z;
+    if (tpr == 0) {  // one chunk of a long row, whole CTA
+        const int row = m.x, chunk = m.y;
+        const int2 lr = __ldg(pl.lrow + m.w);
+        const int kb = __ldg(rp + row) + chunk * kRowChunk;
+        const int e = min(kb + kRowChunk, __ldg(rp + row + 1));
+        double s = 0.0;
+        int k = kb + threadIdx.x;
+        for (; k + 3 * kBlock < e; k += 4 * kBlock) {  // 4 independent gathers in flight per thread
+            int c[4];
+            double a[4];
 #pragma unroll
-    for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o, TPR);
-    if (i < rows && lane == 0) epi.row(i, s, acc);
+            for (int u = 0; u < 4; ++u) {
+                c[u] = __ldg(ci + k + u * kBlock);
+                a[u] = __ldg(v + k + u * kBlock);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s = addd(s, mul(a[u], xf(c[u])));
+        }
+        for (; k < e; k += kBlock) s = addd(s, mul(__ldg(v + k), xf(__ldg(ci + k))));
+        double t[1] = {s};
+        block_sum<1>(t);
+        if (threadIdx.x == 0) {
+            if (lr.y == 1) {
+                epi.row(row, t[0], acc);
+            } else {
+                pl.lpart[lr.x + chunk] = t[0];
+                __threadfence();
+                if (atomicAdd(pl.lcnt + m.w, 1u) == (unsigned)lr.y - 1) {
+                    __threadfence();
+                    double tot = 0.0;
+                    for (int q = 0; q < lr.y; ++q) tot += __ldcg(pl.lpart + lr.x + q);
+                    pl.lcnt[m.w] = 0;
+                    epi.row(row, tot, acc);
+                }
+            }
+        }
+    } else {
+        const int r0 = m.x, r1 = m.y;
+        const int lane = threadIdx.x & (tpr - 1), grp = threadIdx.x / tpr, ngrp = kBlock / tpr;
+        for (int base = r0; base < r1; base += ngrp) {
+            const int i = base + grp;
+            double s = 0.0;
+            if (i < r1) {
+                const int e = __ldg(rp + i + 1);
+                int k = __ldg(rp + i) + lane;
+                for (; k + 3 * tpr < e; k += 4 * tpr) {
+                    int c[4];
+                    double a[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        c[u] = __ldg(ci + k + u * tpr);
+                        a[u] = __ldg(v + k + u * tpr);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) s = addd(s, mul(a[u], xf(c[u])));
+                }
+                for (; k < e; k += tpr) s = addd(s, mul(__ldg(v + k), xf(__ldg(ci + k))));
+            }
+            for (int o = tpr >> 1; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o, tpr);
+            if (i < r1 && lane == 0) epi.row(i, s, acc);
+        }
+    }
     if constexpr (NR > 0) {
         if (grid_sum_last<NR>(acc, epi.slot())) epi.fin(acc);
     }
@@ -180,17 +333,15 @@ template <class XF, class Epi>
 inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
     if (A->rows == 0) return;
     if (A->kind == SPMV_SELL) {
-        const int grid = (A->rows + kBlock - 1) / kBlock;
+        const int grid = (A->rows + kSellRows * kBlock - 1) / (kSellRows * kBlock);
         k_spmv_sell<<<grid, kBlock, 0, s>>>(A->rows, A->rp.p, A->sell_off.p, A->sell_ci.p, A->sell_v.p, xf, epi);
+    } else if (A->kind == SPMV_SELLW) {
+        const int grid = (A->rows + kBlock - 1) / kBlock;
+        k_spmv_sellw<<<grid, kBlock, 0, s>>>(A->rows, A->rp.p, A->perm.p, A->sell_off.p, A->sell_ci.p, A->sell_v.p,
+                                             xf, epi);
     } else {
-        const long long threads = (long long)A->rows * A->tpr;
-        const int grid = (int)((threads + kBlock - 1) / kBlock);
-        switch (A->tpr) {
-            case 4: k_spmv_vec<4><<<grid, kBlock, 0, s>>>(A->rows, A->rp.p, A->ci.p, A->v.p, xf, epi); break;
-            case 8: k_spmv_vec<8><<<grid, kBlock, 0, s>>>(A->rows, A->rp.p, A->ci.p, A->v.p, xf, epi); break;
-            case 16: k_spmv_vec<16><<<grid, kBlock, 0, s>>>(A->rows, A->rp.p, A->ci.p, A->v.p, xf, epi); break;
-            default: k_spmv_vec<32><<<grid, kBlock, 0, s>>>(A->rows, A->rp.p, A->ci.p, A->v.p, xf, epi); break;
-        }
+        const AdaptPlan pl{A->blk_meta.p, A->lrow.p, A->lpart.p, A->lcnt.p};
+        k_spmv_adapt<<<A->n_blocks, kBlock, 0, s>>>(pl, A->rp.p, A->ci.p, A->v.p, xf, epi);
     }
     CK_LAUNCH(c);
 }
@@ -198,8 +349,9 @@ inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
 // Number of blocks launch_spmv uses (sizes the reduction partials).
 inline int spmv_grid(const Mat* A) {
     if (A->rows == 0) return 0;
-    if (A->kind == SPMV_SELL) return (A->rows + kBlock - 1) / kBlock;
-    return (int)(((long long)A->rows * A->tpr + kBlock - 1) / kBlock);
+    if (A->kind == SPMV_SELL) return (A->rows + kSellRows * kBlock - 1) / (kSellRows * kBlock);
+    if (A->kind == SPMV_SELLW) return (A->rows + kBlock - 1) / kBlock;
+    return A->n_blocks;
 }
 
 // Plain epilogue: y_i = s.

@@ -51,7 +51,7 @@ struct EpiInitResidual {  // r_i = b_i - (A x)_i ; reduce b.b and r.r
             S.rel = 0.0;
             S.done = 1;
             S.zero_x = 1;
-            cudaGraphSetConditional(S.cond, 0);
+            if (S.use_cond) cudaGraphSetConditional(S.cond, 0);
             return;
         }
         S.rel = __ddiv_rn(__dsqrt_rn(tot[1]), S.bnorm);
@@ -61,7 +61,7 @@ struct EpiInitResidual {  // r_i = b_i - (A x)_i ; reduce b.b and r.r
             S.status = 0;
             S.iterations = 0;
             S.done = 1;
-            cudaGraphSetConditional(S.cond, 0);
+            if (S.use_cond) cudaGraphSetConditional(S.cond, 0);
         }
     }
 };
@@ -120,6 +120,7 @@ struct EpiSpmvPAp {  // B1
     RedSlot rs;
     PcgState* st;
     __device__ bool skip() const { return st->done != 0; }
+    __device__ void touch(int i) const { pf(p + i); }
     __device__ void row(int i, double s, double* acc) const {
         Ap[i] = s;
         acc[0] += p[i] * s;
@@ -132,7 +133,7 @@ struct EpiSpmvPAp {  // B1
             S.status = 2;
             S.iterations = S.it - 1;
             S.done = 1;
-            cudaGraphSetConditional(S.cond, 0);
+            if (S.use_cond) cudaGraphSetConditional(S.cond, 0);
             return;
         }
         S.alpha = __ddiv_rn(S.rz, S.pAp);
@@ -145,7 +146,7 @@ __device__ __forceinline__ void finish_iteration(PcgState& S) {
         S.status = 1;
         S.iterations = S.max_iters;
         S.done = 1;
-        cudaGraphSetConditional(S.cond, 0);
+        if (S.use_cond) cudaGraphSetConditional(S.cond, 0);
         return;
     }
     ++S.it;
@@ -185,7 +186,7 @@ struct BodyUpdate {  // B2
             S.status = 0;
             S.iterations = S.it;
             S.done = 1;
-            cudaGraphSetConditional(S.cond, 0);
+            if (S.use_cond) cudaGraphSetConditional(S.cond, 0);
             return;
         }
         if (kind != IBMGPU_PC_SA) {
@@ -374,16 +375,30 @@ void PcgPlan::run(Ctx* c, const ibm_solver_params& prm, double* hist_dev) {
     H.max_iters = prm.max_iters;
     H.hist = hist_dev;
     H.cond = cond;
+    H.use_cond = c->eager ? 0 : 1;
     CK(cudaMemcpyAsync(st.p, &H, sizeof(PcgState), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaGraphLaunch(exec, c->stream));
+    last_eager = c->eager != 0;
+    if (!last_eager) {
+        CK(cudaGraphLaunch(exec, c->stream));
+    } else {
+        // Profiling mode (IBMGPU_EAGER=1): the same kernels launched from the host, 8 iterations
+        // between done-flag checks (ncu cannot profile kernel nodes of conditional graphs).
+        enqueue_init(c, c->stream);
+        for (int it = 0; it <= prm.max_iters + 8; it += 8) {
+            for (int k = 0; k < 8; ++k) enqueue_body(c, c->stream);
+            CK(cudaMemcpyAsync(host_st, st.p, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+            sync(c);
+            if (host_st->done) break;
+        }
+    }
     CK(cudaMemcpyAsync(host_st, st.p, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
 }
 
 void PcgPlan::finish(Ctx* c, ibm_solve_result* res) {
     sync(c);
     const PcgState& H = *host_st;
-    // iterations executed: init + one body per started iteration
-    c->launches += kernels_init + (long long)kernels_iter * std::max(H.it, 0);
+    // iterations executed: init + one body per started iteration (eager mode counted at launch)
+    if (!last_eager) c->launches += kernels_init + (long long)kernels_iter * std::max(H.it, 0);
     if (res) {
         res->iterations = H.iterations;
         res->rel_residual = H.rel;

@@ -8,7 +8,7 @@ namespace ibmgpu {
 // Device-resident scalars of one solve (krylov.hpp:91-135 locals + SolveResult fields).
 struct PcgState {
     double bnorm, rel, rel_tol, rz, pAp, alpha, beta;
-    int it, max_iters, status, done, iterations, zero_x, hist_len, pad;
+    int it, max_iters, status, done, iterations, zero_x, hist_len, use_cond;
     double* hist;
     cudaGraphConditionalHandle cond;
 };
@@ -27,6 +27,7 @@ struct PcgPlan {
     cudaGraphExec_t exec = nullptr;
     cudaGraphConditionalHandle cond = 0;
     int kernels_init = 0, kernels_iter = 0;
+    bool last_eager = false;
 
     PcgPlan(Ctx* c, Mat* A, int kind, Hier* h);
     ~PcgPlan();
