@@ -14,6 +14,7 @@
 #include <memory>
 #include <vector>
 
+#include "coarse.cuh"
 #include "internal.cuh"
 #include "kern.cuh"
 
@@ -45,6 +46,11 @@ struct ibmgpu_hier {
     int n_c = 0;
     ibmgpu::DBuf<double> coarse_inv;  // n_c x n_c row-major, symmetric
     ibmgpu::DBuf<double> cb, cx;      // coarse rhs / solution
+    // fused coarse sub-cycle (coarse.cuh): levels [fuse_from, L) + dense solve in one launch
+    int fuse_from = 0;
+    int n_phases = 0, coarse_grid = 0;
+    ibmgpu::DBuf<ibmgpu::Phase> phases;
+    ibmgpu::DBuf<unsigned> bar;       // {count, generation}
     bool stalled = false;
     long long id = 0;
     int built_at_step = -1;
@@ -158,15 +164,22 @@ inline void vcycle_launch(Ctx* c, Hier* h, const double* r_in, double* z_out, co
         launch_dense_gemv(c, h->n_c, h->coarse_inv.p, r_in, z_out, done, s);
         return;
     }
-    for (int l = 0; l < L; ++l) {
+    const int F = h->n_phases ? h->fuse_from : L;  // levels >= F run inside the fused kernel
+    for (int l = 0; l < F; ++l) {
         Level& lv = *h->levels[l];
         const double* b = l == 0 ? r_in : lv.b.p;
         launch_spmv(c, lv.A, XJacobi{lv.wd.p, b}, EpiJacobiResidual{lv.wd.p, b, lv.x.p, lv.r.p, done}, s);
         double* bn = l + 1 < L ? h->levels[l + 1]->b.p : h->cb.p;
         launch_spmv(c, lv.Pt, XPlain{lv.r.p}, EpiStoreSkip{bn, done}, s);
     }
-    launch_dense_gemv(c, h->n_c, h->coarse_inv.p, h->cb.p, h->cx.p, done, s);
-    for (int l = L - 1; l >= 0; --l) {
+    if (F < L) {
+        k_coarse_cycle<<<h->coarse_grid, kBlock, 0, s>>>(CoarsePlan{h->phases.p, h->n_phases, h->bar.p, h->bar.p + 1},
+                                                         done);
+        CK_LAUNCH(c);
+    } else {
+        launch_dense_gemv(c, h->n_c, h->coarse_inv.p, h->cb.p, h->cx.p, done, s);
+    }
+    for (int l = F - 1; l >= 0; --l) {
         Level& lv = *h->levels[l];
         const double* b = l == 0 ? r_in : lv.b.p;
         const double* ec = l + 1 < L ? h->levels[l + 1]->xo.p : h->cx.p;
@@ -190,6 +203,10 @@ struct LastPlain {
 };
 
 // kernels launched by one V-cycle (for launch accounting)
-inline int vcycle_kernels(const Hier* h) { return h->levels.empty() ? 1 : 4 * (int)h->levels.size() + 1; }
+inline int vcycle_kernels(const Hier* h) {
+    if (h->levels.empty()) return 1;
+    const int F = h->n_phases ? h->fuse_from : (int)h->levels.size();
+    return 4 * F + 1;
+}
 
 }  // namespace ibmgpu

@@ -17,6 +17,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 
 #include "amg.cuh"
 #include "internal.cuh"
@@ -287,6 +288,70 @@ double rho_dinv_a(Ctx* c, Mat* A, const double* invd, int iters) {
     return h.zero ? 1.0 : h.lambda;
 }
 
+// Fused coarse sub-cycle (coarse.cuh): every level from the first one whose operator is small
+// enough (<= kFuseRows rows) down to the dense solve runs in one persistent launch. Level 0 is
+// never fused (its post-smoother carries the PCG's fused r.z reduction).
+constexpr int kFuseRows = 0;  // measured slower than separate graph launches on B200; opt in via IBMGPU_FUSE_ROWS
+
+void build_fused_coarse(Ctx* c, Hier* h) {
+    const int L = (int)h->levels.size();
+    const char* ev = std::getenv("IBMGPU_FUSE_ROWS");
+    const int fuse_rows = ev ? std::atoi(ev) : kFuseRows;
+    const char* ec = std::getenv("IBMGPU_FUSE_CTAS");
+    const int ctas_per_sm = ec ? std::max(1, std::atoi(ec)) : 1;
+    int F = L;
+    while (F > 1 && h->levels[F - 1]->A->rows <= fuse_rows) --F;
+    if (F >= L) return;
+    std::vector<Phase> ph;
+    auto spmv_phase = [&](int kind, Mat* M) {
+        mat_plan_adaptive(c, M);
+        Phase p{};
+        p.kind = kind;
+        p.n_blocks = M->n_blocks;
+        p.pl = AdaptPlan{M->blk_meta.p, M->lrow.p, M->lpart.p, M->lcnt.p};
+        p.rp = M->rp.p;
+        p.ci = M->ci.p;
+        p.v = M->v.p;
+        return p;
+    };
+    for (int l = F; l < L; ++l) {
+        Level& lv = *h->levels[l];
+        Phase k1 = spmv_phase(PH_JACOBI, lv.A);
+        k1.wd = lv.wd.p, k1.b = lv.b.p, k1.x = lv.x.p, k1.out = lv.r.p;
+        ph.push_back(k1);
+        Phase k2 = spmv_phase(PH_STORE, lv.Pt);
+        k2.x = lv.r.p, k2.out = l + 1 < L ? h->levels[l + 1]->b.p : h->cb.p;
+        ph.push_back(k2);
+    }
+    Phase g{};
+    g.kind = PH_GEMV;
+    g.n_blocks = h->n_c;
+    g.v = h->coarse_inv.p;
+    g.x = h->cb.p;
+    g.out = h->cx.p;
+    ph.push_back(g);
+    for (int l = L - 1; l >= F; --l) {
+        Level& lv = *h->levels[l];
+        Phase k3 = spmv_phase(PH_ADD, lv.P);
+        k3.x = l + 1 < L ? h->levels[l + 1]->xo.p : h->cx.p;
+        k3.out = lv.x.p;
+        ph.push_back(k3);
+        Phase k4 = spmv_phase(PH_POST, lv.A);
+        k4.wd = lv.wd.p, k4.b = lv.b.p, k4.x = lv.x.p, k4.out = lv.xo.p;
+        ph.push_back(k4);
+    }
+    h->fuse_from = F;
+    h->n_phases = (int)ph.size();
+    h->phases.alloc(c, ph.size());
+    h2d(c, h->phases.p, ph.data(), ph.size());
+    h->bar.alloc(c, 2);
+    CK(cudaMemsetAsync(h->bar.p, 0, 2 * sizeof(unsigned), c->stream));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_cycle, kBlock, 0));
+    // every CTA must be co-resident for the software grid barrier
+    h->coarse_grid = std::max(1, std::min(per_sm, ctas_per_sm) * c->num_sms);
+}
+
 }  // namespace
 
 // Strength graph + exact greedy aggregation; returns aggregate count, agg sized n_core.
@@ -443,6 +508,7 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
         dense_spd_inverse(c, h->coarse_A, h->coarse_inv.p);
         h->cb.alloc(c, (size_t)h->n_c);
         h->cx.alloc(c, (size_t)h->n_c);
+        build_fused_coarse(c, h);
         sync(c);
     } catch (...) {
         delete h;

@@ -11,6 +11,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.cuh"
 #include "kern.cuh"
@@ -89,6 +90,134 @@ __global__ void k_sell_fill(int rows, const int* __restrict__ rp, const int* __r
     }
 }
 
+// ---- stencil (DIA-hybrid) plan: classify each row against the band {i-S,i-1,i,i+1,i+S}
+__device__ bool band_match(int i, int b, int e, const int* __restrict__ ci, int S, unsigned& mask, int& ext) {
+    const int col[5] = {i - S, i - 1, i, i + 1, i + S};
+    mask = 0;
+    int q = 0;
+    for (int k = b; k < e; ++k) {
+        const int c = ci[k];
+        if (c > i + S) {
+            ext = k;
+            return true;
+        }
+        while (q < 5 && col[q] < c) ++q;
+        if (q < 5 && col[q] == c) {
+            mask |= 1u << q;
+            ++q;
+        } else {
+            return false;
+        }
+    }
+    ext = e;
+    return true;
+}
+
+__global__ void k_stencil_classify(int rows, const int* __restrict__ rp, const int* __restrict__ ci, int S1, int S2,
+                                   unsigned char* __restrict__ mask, int* __restrict__ estart,
+                                   int* __restrict__ ecount) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const int b = rp[i], e = rp[i + 1];
+    unsigned m = 0;
+    int ext = b;
+    if (band_match(i, b, e, ci, S1, m, ext)) {
+    } else if (S2 > 1 && band_match(i, b, e, ci, S2, m, ext)) {
+        m |= 64u;
+    } else {
+        m = 0;  // generic row: every entry goes to the CSR tail
+        ext = b;
+    }
+    if (e > ext) m |= 32u;
+    mask[i] = static_cast<unsigned char>(m);
+    estart[i] = ext;
+    ecount[i] = e - ext;
+}
+
+__global__ void k_stencil_fill(int rows, const int* __restrict__ rp, const int* __restrict__ ci,
+                               const double* __restrict__ v, int S1, int S2, const unsigned char* __restrict__ mask,
+                               const int* __restrict__ estart, const int* __restrict__ erp, double* __restrict__ sv,
+                               int* __restrict__ eci, double* __restrict__ ev) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    const unsigned m = mask[i];
+    const int S = (m & 64u) ? S2 : S1;
+    const int col[5] = {i - S, i - 1, i, i + 1, i + S};
+    const int b = rp[i], ext = estart[i];
+    int k = b;
+    for (int q = 0; q < 5; ++q) {
+        double val = 0.0;
+        if (m & (1u << q)) {
+            while (k < ext && ci[k] != col[q]) ++k;
+            val = v[k++];
+        }
+        sv[(size_t)q * rows + i] = val;
+    }
+    const int o = erp[i];
+    for (int kk = ext; kk < rp[i + 1]; ++kk) {
+        eci[o + kk - ext] = ci[kk];
+        ev[o + kk - ext] = v[kk];
+    }
+}
+
+// two most frequent positive offsets > 1 among sampled rows (grid strides of the 5-point blocks)
+void detect_strides(Ctx* c, const Mat* m, int& S1, int& S2) {
+    S1 = S2 = 0;
+    std::vector<std::pair<int, int>> hist;  // (offset, count)
+    const int win = std::min(m->rows, 2048);
+    for (const double f : {0.0, 0.5, 0.8}) {
+        const int r0 = std::min(m->rows - win, static_cast<int>(f * m->rows));
+        std::vector<int> rp(static_cast<size_t>(win) + 1);
+        d2h(c, rp.data(), m->rp.p + r0, rp.size());
+        sync(c);
+        const int n = rp[win] - rp[0];
+        std::vector<int> ci(static_cast<size_t>(std::max(n, 1)));
+        d2h(c, ci.data(), m->ci.p + rp[0], (size_t)n);
+        sync(c);
+        for (int r = 0; r < win; ++r)
+            for (int k = rp[r] - rp[0]; k < rp[r + 1] - rp[0]; ++k) {
+                const int off = ci[k] - (r0 + r);
+                if (off <= 1) continue;
+                auto it = std::find_if(hist.begin(), hist.end(), [&](auto& p) { return p.first == off; });
+                if (it == hist.end()) hist.push_back({off, 1});
+                else ++it->second;
+            }
+    }
+    std::sort(hist.begin(), hist.end(), [](auto& a, auto& b) { return a.second > b.second; });
+    const int thresh = win / 8;  // a stride must appear in >= 1/8 of one window's rows
+    if (hist.size() > 0 && hist[0].second >= thresh) S1 = hist[0].first;
+    if (hist.size() > 1 && hist[1].second >= thresh) S2 = hist[1].first;
+}
+
+// Build the stencil plan if >= 90% of the nonzeros sit in the band; returns true on success.
+bool try_stencil(Ctx* c, Mat* m) {
+    if (m->rows != m->cols || m->rows < 4096) return false;
+    int S1, S2;
+    detect_strides(c, m, S1, S2);
+    if (S1 <= 1) return false;
+    const int n = m->rows;
+    DBuf<unsigned char> mask(c, (size_t)n);
+    DBuf<int> estart(c, (size_t)n), ecount(c, (size_t)n), erp(c, (size_t)n + 1);
+    k_stencil_classify<<<(n + 255) / 256, 256, 0, c->stream>>>(n, m->rp.p, m->ci.p, S1, S2, mask.p, estart.p, ecount.p);
+    CK_LAUNCH(c);
+    exclusive_scan_total(c, ecount.p, erp.p, n);
+    const int n_ext = d2h_scalar(c, erp.p + n);
+    if (n_ext > m->nnz / 10) return false;
+    m->st_S1 = S1;
+    m->st_S2 = S2;
+    m->st_v.alloc(c, (size_t)5 * n);
+    m->st_eci.alloc(c, (size_t)std::max(n_ext, 1));
+    m->st_ev.alloc(c, (size_t)std::max(n_ext, 1));
+    k_stencil_fill<<<(n + 255) / 256, 256, 0, c->stream>>>(n, m->rp.p, m->ci.p, m->v.p, S1, S2, mask.p, estart.p, erp.p,
+                                                           m->st_v.p, m->st_eci.p, m->st_ev.p);
+    CK_LAUNCH(c);
+    m->st_mask = std::move(mask);
+    m->st_erp = std::move(erp);
+    m->kind = SPMV_STENCIL;
+    sync(c);
+    return true;
+}
+
 __global__ void k_diag(int n, const int* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ v,
                        double* __restrict__ d) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -125,6 +254,7 @@ void mat_plan(Ctx* c, Mat* m) {
     CK_LAUNCH(c);
     m->max_row = d2h_scalar(c, mx.p);
     const double avg = m->rows ? double(m->nnz) / m->rows : 0.0;
+    if (avg <= 12.0 && !std::getenv("IBMGPU_NO_STENCIL") && try_stencil(c, m)) return;
     if (avg <= 12.0 && m->max_row <= 48) {
         m->kind = SPMV_SELL;
         m->sell_off.alloc(c, (size_t)n_slices + 1);
@@ -175,9 +305,22 @@ void mat_plan(Ctx* c, Mat* m) {
             return;
         }
     }
+    m->kind = SPMV_VECTOR;
+    plan_adaptive_from(c, m, rp);
+}
+
+void mat_plan_adaptive(Ctx* c, Mat* m) {
+    if (m->n_blocks > 0 || m->rows == 0) return;
+    std::vector<int> rp(static_cast<size_t>(m->rows) + 1);
+    d2h(c, rp.data(), m->rp.p, rp.size());
+    sync(c);
+    plan_adaptive_from(c, m, rp);
+}
+
+// CSR-adaptive chunks (kern.cuh k_spmv_adapt / coarse.cuh), planned on the host from row_ptr
+void plan_adaptive_from(Ctx* c, Mat* m, const std::vector<int>& rp) {
+    const double avg = m->rows ? double(m->nnz) / m->rows : 0.0;
     {
-        // CSR-adaptive chunks (kern.cuh k_spmv_adapt), planned on the host from row_ptr
-        m->kind = SPMV_VECTOR;
         constexpr int kChunkNnz = 2048;
         // rows much longer than the mean never share a CTA with short rows
         const int kOwnCta = std::max(128, static_cast<int>(4.0 * avg));

@@ -114,7 +114,7 @@ inline T d2h_scalar(Ctx* c, const T* src) {
 }
 
 // SpMV execution plan chosen at construction from the row-length profile.
-enum SpmvKind { SPMV_SELL = 0, SPMV_VECTOR = 1, SPMV_SELLW = 2 };
+enum SpmvKind { SPMV_SELL = 0, SPMV_VECTOR = 1, SPMV_SELLW = 2, SPMV_STENCIL = 3 };
 
 }  // namespace ibmgpu
 
@@ -132,6 +132,14 @@ struct ibmgpu_mat {
     ibmgpu::DBuf<int> sell_ci;
     ibmgpu::DBuf<double> sell_v;
     ibmgpu::DBuf<int> perm;              // SELL-sigma: slot -> original row
+    // stencil (DIA-hybrid) plan: 5-point band {i-S, i-1, i, i+1, i+S} as 5 value planes + a
+    // per-row presence mask (bit 6 selects the second stride), extras (columns > i+S, or whole
+    // rows that do not fit the band) in a CSR tail — summation order equals CSR column order
+    int st_S1 = 0, st_S2 = 0;
+    ibmgpu::DBuf<double> st_v;           // 5 * rows, plane-major
+    ibmgpu::DBuf<unsigned char> st_mask; // rows
+    ibmgpu::DBuf<int> st_erp, st_eci;    // extras CSR
+    ibmgpu::DBuf<double> st_ev;
     int n_blocks = 0;                   // CSR-adaptive plan (kern.cuh k_spmv_adapt)
     ibmgpu::DBuf<int4> blk_meta;         // per CTA: {r0, r1, tpr, 0} | {row, chunk, 0, long-row id}
     ibmgpu::DBuf<int2> lrow;             // per long row: {partial base, chunks}
@@ -147,6 +155,8 @@ using Mat = ibmgpu_mat;
 // csr.cu
 Mat* mat_new(Ctx* c, int rows, int cols, int nnz);
 void mat_plan(Ctx* c, Mat* m);              // build the SpMV plan (SELL copy or vector width)
+void mat_plan_adaptive(Ctx* c, Mat* m);     // CSR-adaptive chunk plan (also used by the fused coarse cycle)
+void plan_adaptive_from(Ctx* c, Mat* m, const std::vector<int>& rp);
 void spmv(Ctx* c, Mat* A, const double* x, double* y);
 Mat* mat_upload(Ctx* c, int rows, int cols, int nnz, const int* rp, const int* ci, const double* v);
 void mat_download(Ctx* c, const Mat* m, int* rp, int* ci, double* v);

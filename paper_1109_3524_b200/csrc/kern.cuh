@@ -174,6 +174,58 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
     }
 }
 
+// Stencil (DIA-hybrid) SpMV for the 5-point operators (lhs2 / level-0 A, the velocity A and L):
+// thread per row, every load coalesced and independent of any index stream — the five band
+// values, the mask byte and x[i-S], x[i-1], x[i], x[i+1], x[i+S] all issue at once; only rows
+// with extras (body coupling, pinned row) touch the CSR tail. Band slots are summed in column
+// order, then the extras (whose columns all exceed i+S), so rounding equals spmv_into.
+struct StencilPlan {
+    const double* v;            // 5 planes of n
+    const unsigned char* mask;  // bits 0-4 slot present, bit 5 has extras, bit 6 second stride
+    const int* erp;
+    const int* eci;
+    const double* ev;
+    int S1, S2;
+};
+
+template <class XF, class Epi>
+__global__ void __launch_bounds__(kBlock) k_spmv_stencil(int rows, StencilPlan P, XF xf, Epi epi) {
+    constexpr int NR = Epi::NR;
+    if (epi.skip()) return;
+    double acc[NR > 0 ? NR : 1];
+#pragma unroll
+    for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
+    const int i = blockIdx.x * kBlock + threadIdx.x;
+    const bool live = i < rows;
+    const unsigned m = live ? __ldg(P.mask + i) : 0u;
+    if constexpr (requires { epi.touch(0); }) {
+        if (live) epi.touch(i);
+    }
+    const int S = (m & 64u) ? P.S2 : P.S1;
+    double a[5], xv[5];
+    const int col[5] = {i - S, i - 1, i, i + 1, i + S};
+#pragma unroll
+    for (int q = 0; q < 5; ++q)
+        if (m & (1u << q)) {
+            a[q] = __ldg(P.v + (size_t)q * rows + i);
+            xv[q] = xf(col[q]);
+        }
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 5; ++q)
+        if (m & (1u << q)) s = addd(s, mul(a[q], xv[q]));
+    if (__any_sync(kFull, m & 32u)) {
+        if (m & 32u) {
+            const int e = __ldg(P.erp + i + 1);
+            for (int k = __ldg(P.erp + i); k < e; ++k) s = addd(s, mul(__ldg(P.ev + k), xf(__ldg(P.eci + k))));
+        }
+    }
+    if (live) epi.row(i, s, acc);
+    if constexpr (NR > 0) {
+        if (grid_sum_last<NR>(acc, epi.slot())) epi.fin(acc);
+    }
+}
+
 // SELL-32-sigma for the wider Galerkin levels (15-60 entries per row): rows are sorted by length
 // (descending) within 512-row windows so a slice's rows have similar lengths, slot i holds
 // original row perm[i]. Entries keep their column order, so the sum is still bit-exact with
@@ -335,6 +387,9 @@ inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
     if (A->kind == SPMV_SELL) {
         const int grid = (A->rows + kSellRows * kBlock - 1) / (kSellRows * kBlock);
         k_spmv_sell<<<grid, kBlock, 0, s>>>(A->rows, A->rp.p, A->sell_off.p, A->sell_ci.p, A->sell_v.p, xf, epi);
+    } else if (A->kind == SPMV_STENCIL) {
+        const StencilPlan P{A->st_v.p, A->st_mask.p, A->st_erp.p, A->st_eci.p, A->st_ev.p, A->st_S1, A->st_S2};
+        k_spmv_stencil<<<(A->rows + kBlock - 1) / kBlock, kBlock, 0, s>>>(A->rows, P, xf, epi);
     } else if (A->kind == SPMV_SELLW) {
         const int grid = (A->rows + kBlock - 1) / kBlock;
         k_spmv_sellw<<<grid, kBlock, 0, s>>>(A->rows, A->rp.p, A->perm.p, A->sell_off.p, A->sell_ci.p, A->sell_v.p,
@@ -350,7 +405,7 @@ inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
 inline int spmv_grid(const Mat* A) {
     if (A->rows == 0) return 0;
     if (A->kind == SPMV_SELL) return (A->rows + kSellRows * kBlock - 1) / (kSellRows * kBlock);
-    if (A->kind == SPMV_SELLW) return (A->rows + kBlock - 1) / kBlock;
+    if (A->kind == SPMV_SELLW || A->kind == SPMV_STENCIL) return (A->rows + kBlock - 1) / kBlock;
     return A->n_blocks;
 }
 

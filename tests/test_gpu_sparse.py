@@ -113,3 +113,13 @@ def test_empty_and_ragged():
     assert (T.rows(), T.cols(), T.nnz()) == (3, 4, 0)
     R = ibm.SparseMatrix.from_triplets(5, 5, [(0, 4, 1.0), (4, 0, 2.0)])
     assert np.array_equal(R.spmv(np.arange(5.0)), [4.0, 0, 0, 0, 0])
+
+
+@pytest.mark.parametrize("op", ["lhs2", "A", "L", "QT"])
+def test_stencil_format_spmv_bitwise(port, ref, op):
+    """Stencil (DIA-hybrid) plan on the 330^2 case operators: lhs2 (one stride + body extras and
+    generic body rows), A and L (two strides: u rows nx-1, v rows nx). Bit-exact vs spmv_into."""
+    c = ref.case(H.case("cylinder_re40"))
+    m = c.op(op)
+    x = np.cos(np.arange(m.cols) * 0.61 + 0.2)
+    assert np.array_equal(dev(m).spmv(x), port.spmv(m, x))
