@@ -45,6 +45,7 @@ struct ibmgpu_hier {
     ibmgpu::Mat* coarse_A = nullptr;
     int n_c = 0;
     ibmgpu::DBuf<double> coarse_inv;  // n_c x n_c row-major, symmetric
+    ibmgpu::DBuf<double> coarse_tiles, prow, pcol;  // packed lower-triangle tiles + SYMV partials
     ibmgpu::DBuf<double> cb, cx;      // coarse rhs / solution
     // fused coarse sub-cycle (coarse.cuh): levels [fuse_from, L) + dense solve in one launch
     int fuse_from = 0;
@@ -67,6 +68,16 @@ int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& 
 void dense_spd_inverse(Ctx* c, const Mat* Ac, double* inv);  // factor (dense.hpp:20-40) + inverse
 void launch_dense_gemv(Ctx* c, int n, const double* Ainv, const double* x, double* y, const int* done,
                        cudaStream_t s);
+void pack_symmetric_tiles(Ctx* c, int n, const double* full, double* tiles);
+size_t packed_tiles_doubles(int n);
+size_t packed_partials_doubles(int n);
+void launch_symv_packed(Ctx* c, int n, const double* tiles, const double* x, double* y, double* prow, double* pcol,
+                        const int* done, cudaStream_t s);
+
+// coarsest level: y = A_c^{-1} x from the packed symmetric inverse (each element read once)
+inline void coarse_solve(Ctx* c, Hier* h, const double* x, double* y, const int* done, cudaStream_t s) {
+    launch_symv_packed(c, h->n_c, h->coarse_tiles.p, x, y, h->prow.p, h->pcol.p, done, s);
+}
 
 // ---------------------------------------------------------------- V-cycle epilogues
 struct EpiJacobiResidual {  // K1: x_i = wd_i b_i ; r_i = b_i - s
@@ -161,7 +172,7 @@ inline void vcycle_launch(Ctx* c, Hier* h, const double* r_in, double* z_out, co
                           cudaStream_t s) {
     const int L = (int)h->levels.size();
     if (L == 0) {
-        launch_dense_gemv(c, h->n_c, h->coarse_inv.p, r_in, z_out, done, s);
+        coarse_solve(c, h, r_in, z_out, done, s);
         return;
     }
     const int F = h->n_phases ? h->fuse_from : L;  // levels >= F run inside the fused kernel
@@ -177,7 +188,7 @@ inline void vcycle_launch(Ctx* c, Hier* h, const double* r_in, double* z_out, co
                                                          done);
         CK_LAUNCH(c);
     } else {
-        launch_dense_gemv(c, h->n_c, h->coarse_inv.p, h->cb.p, h->cx.p, done, s);
+        coarse_solve(c, h, h->cb.p, h->cx.p, done, s);
     }
     for (int l = F - 1; l >= 0; --l) {
         Level& lv = *h->levels[l];

@@ -506,6 +506,10 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
         }
         h->coarse_inv.alloc(c, (size_t)h->n_c * h->n_c);
         dense_spd_inverse(c, h->coarse_A, h->coarse_inv.p);
+        h->coarse_tiles.alloc(c, packed_tiles_doubles(h->n_c));
+        h->prow.alloc(c, packed_partials_doubles(h->n_c));
+        h->pcol.alloc(c, packed_partials_doubles(h->n_c));
+        pack_symmetric_tiles(c, h->n_c, h->coarse_inv.p, h->coarse_tiles.p);
         h->cb.alloc(c, (size_t)h->n_c);
         h->cx.alloc(c, (size_t)h->n_c);
         build_fused_coarse(c, h);

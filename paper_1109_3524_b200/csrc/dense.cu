@@ -213,7 +213,98 @@ __global__ void __launch_bounds__(256) k_gemv(int n, const double* __restrict__ 
     if (lane == 0) y[warp] = s;
 }
 
+// ---- packed symmetric inverse: lower-triangle 64x64 tiles, tile (I,J), J <= I, at I(I+1)/2+J
+constexpr int TS = 64;
+
+__global__ void k_pack_tiles(int n, const double* __restrict__ full, double* __restrict__ tiles) {
+    const int t = blockIdx.x;
+    int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    while (I * (I + 1) / 2 > t) --I;
+    const int J = t - I * (I + 1) / 2;
+    double* dst = tiles + (size_t)t * TS * TS;
+    for (int e = threadIdx.x; e < TS * TS; e += blockDim.x) {
+        const int r = I * TS + e / TS, cc = J * TS + e % TS;
+        dst[e] = (r < n && cc < n) ? full[(size_t)r * n + cc] : 0.0;
+    }
+}
+
+// one CTA per tile: row sums A_IJ x_J and (off-diagonal tiles) column sums A_IJ^T x_I, each in a
+// fixed order, from one read of the tile
+__global__ void __launch_bounds__(256) k_symv_tiles(int n, int nt, const double* __restrict__ tiles,
+                                                    const double* __restrict__ x, double* __restrict__ prow,
+                                                    double* __restrict__ pcol, const int* done) {
+    if (done && *(volatile const int*)done) return;
+    __shared__ double A[TS][TS + 1];
+    __shared__ double xi[TS], xj[TS];
+    const int t = blockIdx.x;
+    int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((I + 1) * (I + 2) / 2 <= t) ++I;
+    while (I * (I + 1) / 2 > t) --I;
+    const int J = t - I * (I + 1) / 2;
+    const double* src = tiles + (size_t)t * TS * TS;
+    for (int e = threadIdx.x; e < TS * TS; e += blockDim.x) A[e / TS][e % TS] = __ldg(src + e);
+    if (threadIdx.x < TS) {
+        const int gi = I * TS + threadIdx.x, gj = J * TS + threadIdx.x;
+        xi[threadIdx.x] = gi < n ? x[gi] : 0.0;
+        xj[threadIdx.x] = gj < n ? x[gj] : 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x < TS) {
+        const int r = threadIdx.x;
+        double s = 0.0;
+        for (int k = 0; k < TS; ++k) s += A[r][k] * xj[k];
+        prow[(size_t)t * TS + r] = s;
+    } else if (threadIdx.x < 2 * TS && I != J) {
+        const int cc = threadIdx.x - TS;
+        double s = 0.0;
+        for (int k = 0; k < TS; ++k) s += A[k][cc] * xi[k];
+        pcol[(size_t)t * TS + cc] = s;
+    }
+}
+
+// y_I = sum_{J<=I} prow[(I,J)] + sum_{K>I} pcol[(K,I)], fixed order
+__global__ void k_symv_combine(int n, int nt, const double* __restrict__ prow, const double* __restrict__ pcol,
+                               double* __restrict__ y, const int* done) {
+    if (done && *(volatile const int*)done) return;
+    const int I = blockIdx.x, r = threadIdx.x;
+    if (r >= TS) return;
+    double s = 0.0;
+    for (int J = 0; J <= I; ++J) s += prow[((size_t)I * (I + 1) / 2 + J) * TS + r];
+    for (int K = I + 1; K < nt; ++K) s += pcol[((size_t)K * (K + 1) / 2 + I) * TS + r];
+    const int gi = I * TS + r;
+    if (gi < n) y[gi] = s;
+}
+
 }  // namespace
+
+void pack_symmetric_tiles(Ctx* c, int n, const double* full, double* tiles) {
+    const int nt = (n + TS - 1) / TS;
+    const int ntiles = nt * (nt + 1) / 2;
+    if (ntiles == 0) return;
+    k_pack_tiles<<<ntiles, 256, 0, c->stream>>>(n, full, tiles);
+    CK_LAUNCH(c);
+}
+
+size_t packed_tiles_doubles(int n) {
+    const size_t nt = (size_t)(n + TS - 1) / TS;
+    return nt * (nt + 1) / 2 * TS * TS;
+}
+size_t packed_partials_doubles(int n) {
+    const size_t nt = (size_t)(n + TS - 1) / TS;
+    return nt * (nt + 1) / 2 * TS;
+}
+
+void launch_symv_packed(Ctx* c, int n, const double* tiles, const double* x, double* y, double* prow, double* pcol,
+                        const int* done, cudaStream_t s) {
+    const int nt = (n + TS - 1) / TS;
+    const int ntiles = nt * (nt + 1) / 2;
+    if (ntiles == 0) return;
+    k_symv_tiles<<<ntiles, 256, 0, s>>>(n, nt, tiles, x, prow, pcol, done);
+    CK_LAUNCH(c);
+    k_symv_combine<<<nt, TS, 0, s>>>(n, nt, prow, pcol, y, done);
+    CK_LAUNCH(c);
+}
 
 void dense_spd_inverse(Ctx* c, const Mat* Ac, double* inv) {
     const int n = Ac->rows;

@@ -299,7 +299,7 @@ void PcgPlan::enqueue_init(Ctx* c, cudaStream_t s) {
     launch_elem(c, n, eg, BodyZeroX{x.p, S}, s);
     if (kind == IBMGPU_PC_SA) {
         if (h->levels.empty()) {
-            launch_dense_gemv(c, h->n_c, h->coarse_inv.p, r.p, z.p, done, s);
+            coarse_solve(c, h, r.p, z.p, done, s);
             launch_elem(c, n, eg, BodyDotAfterCoarse<FinInitRz>{r.p, z.p, done, rs, FinInitRz{S}}, s);
         } else {
             vcycle_launch(c, h, r.p, z.p, done, LastDot<FinInitRz>{c, done, rs, FinInitRz{S}, s}, s);
@@ -321,7 +321,7 @@ void PcgPlan::enqueue_body(Ctx* c, cudaStream_t s) {
                 BodyUpdate{x.p, r.p, p.p, Ap.p, kind == IBMGPU_PC_DIAGONAL ? invd.p : nullptr, z.p, kind, rs, S}, s);
     if (kind == IBMGPU_PC_SA) {
         if (h->levels.empty()) {
-            launch_dense_gemv(c, h->n_c, h->coarse_inv.p, r.p, z.p, done, s);
+            coarse_solve(c, h, r.p, z.p, done, s);
             launch_elem(c, n, eg, BodyDotAfterCoarse<FinBeta>{r.p, z.p, done, rs, FinBeta{S}}, s);
         } else {
             vcycle_launch(c, h, r.p, z.p, done, LastDot<FinBeta>{c, done, rs, FinBeta{S}, s}, s);
