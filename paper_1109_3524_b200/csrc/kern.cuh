@@ -96,6 +96,46 @@ __device__ __forceinline__ bool grid_sum_last(double (&v)[NR], RedSlot slot) {
     return threadIdx.x == 0;
 }
 
+// Per-block partial only (no fence, no atomic): the grid total is formed by k_finalize, launched
+// right after on the same stream — the kernel boundary provides visibility. (A per-block
+// __threadfence + arrival atomic costs ~40% of a 16k-block SpMV on B200: the SC fence also
+// invalidates the SM's L1, evicting co-resident blocks' gather reuse.)
+template <int NR>
+__device__ __forceinline__ void block_partial(double (&v)[NR], RedSlot slot) {
+    block_sum<NR>(v);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int r = 0; r < NR; ++r) slot.partials[(size_t)blockIdx.x * NR + r] = v[r];
+}
+
+// One CTA: sum the partials of `nblocks` blocks in a fixed order and run epi.fin(tot).
+template <class Epi>
+__global__ void __launch_bounds__(256) k_finalize(Epi epi, int nblocks) {
+    constexpr int NR = Epi::NR;
+    if (epi.skip()) return;
+    const RedSlot slot = epi.slot();
+    double t[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) t[r] = 0.0;
+    int b = threadIdx.x;
+    for (; b + 768 < nblocks; b += 1024) {  // 4 independent loads in flight per thread
+        double u[4][NR];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int r = 0; r < NR; ++r) u[q][r] = slot.partials[(size_t)(b + 256 * q) * NR + r];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int r = 0; r < NR; ++r) t[r] += u[q][r];
+    }
+    for (; b < nblocks; b += 256)
+#pragma unroll
+        for (int r = 0; r < NR; ++r) t[r] += slot.partials[(size_t)b * NR + r];
+    block_sum<NR>(t);
+    if (threadIdx.x == 0) epi.fin(t);
+}
+
 // ---------------------------------------------------------------- operand gathers
 struct XPlain {
     const double* x;
@@ -170,7 +210,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
     for (int q = 0; q < kSellRows; ++q)
         if (ix[q] < rows) epi.row(ix[q], s[q], acc);
     if constexpr (NR > 0) {
-        if (grid_sum_last<NR>(acc, epi.slot())) epi.fin(acc);
+        block_partial<NR>(acc, epi.slot());
     }
 }
 
@@ -222,7 +262,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_stencil(int rows, StencilPlan P
     }
     if (live) epi.row(i, s, acc);
     if constexpr (NR > 0) {
-        if (grid_sum_last<NR>(acc, epi.slot())) epi.fin(acc);
+        block_partial<NR>(acc, epi.slot());
     }
 }
 
@@ -282,7 +322,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_spmv_sellw(int rows, const int* _
     }
     if (row >= 0) epi.row(row, s, acc);
     if constexpr (NR > 0) {
-        if (grid_sum_last<NR>(acc, epi.slot())) epi.fin(acc);
+        block_partial<NR>(acc, epi.slot());
     }
 }
 
@@ -376,7 +416,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_adapt(AdaptPlan pl, const int* 
         }
     }
     if constexpr (NR > 0) {
-        if (grid_sum_last<NR>(acc, epi.slot())) epi.fin(acc);
+        block_partial<NR>(acc, epi.slot());
     }
 }
 
@@ -384,21 +424,28 @@ __global__ void __launch_bounds__(kBlock) k_spmv_adapt(AdaptPlan pl, const int* 
 template <class XF, class Epi>
 inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
     if (A->rows == 0) return;
+    int grid = 0;
     if (A->kind == SPMV_SELL) {
-        const int grid = (A->rows + kSellRows * kBlock - 1) / (kSellRows * kBlock);
+        grid = (A->rows + kSellRows * kBlock - 1) / (kSellRows * kBlock);
         k_spmv_sell<<<grid, kBlock, 0, s>>>(A->rows, A->rp.p, A->sell_off.p, A->sell_ci.p, A->sell_v.p, xf, epi);
     } else if (A->kind == SPMV_STENCIL) {
         const StencilPlan P{A->st_v.p, A->st_mask.p, A->st_erp.p, A->st_eci.p, A->st_ev.p, A->st_S1, A->st_S2};
-        k_spmv_stencil<<<(A->rows + kBlock - 1) / kBlock, kBlock, 0, s>>>(A->rows, P, xf, epi);
+        grid = (A->rows + kBlock - 1) / kBlock;
+        k_spmv_stencil<<<grid, kBlock, 0, s>>>(A->rows, P, xf, epi);
     } else if (A->kind == SPMV_SELLW) {
-        const int grid = (A->rows + kBlock - 1) / kBlock;
+        grid = (A->rows + kBlock - 1) / kBlock;
         k_spmv_sellw<<<grid, kBlock, 0, s>>>(A->rows, A->rp.p, A->perm.p, A->sell_off.p, A->sell_ci.p, A->sell_v.p,
                                              xf, epi);
     } else {
         const AdaptPlan pl{A->blk_meta.p, A->lrow.p, A->lpart.p, A->lcnt.p};
-        k_spmv_adapt<<<A->n_blocks, kBlock, 0, s>>>(pl, A->rp.p, A->ci.p, A->v.p, xf, epi);
+        grid = A->n_blocks;
+        k_spmv_adapt<<<grid, kBlock, 0, s>>>(pl, A->rp.p, A->ci.p, A->v.p, xf, epi);
     }
     CK_LAUNCH(c);
+    if constexpr (Epi::NR > 0) {
+        k_finalize<<<1, 256, 0, s>>>(epi, grid);
+        CK_LAUNCH(c);
+    }
 }
 
 // Number of blocks launch_spmv uses (sizes the reduction partials).
@@ -428,9 +475,7 @@ __global__ void __launch_bounds__(kBlock) k_elem(int n, Body body) {
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
     for (int i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) body.row(i, acc);
-    if constexpr (NR > 0) {
-        if (grid_sum_last<NR>(acc, body.slot())) body.fin(acc);
-    }
+    if constexpr (NR > 0) block_partial<NR>(acc, body.slot());
 }
 
 inline int elem_grid(Ctx* c, long long n) {
@@ -443,6 +488,10 @@ template <class Body>
 inline void launch_elem(Ctx* c, int n, int grid, Body body, cudaStream_t s) {
     k_elem<<<grid, kBlock, 0, s>>>(n, body);
     CK_LAUNCH(c);
+    if constexpr (Body::NR > 0) {
+        k_finalize<<<1, 256, 0, s>>>(body, grid);
+        CK_LAUNCH(c);
+    }
 }
 
 }  // namespace ibmgpu
