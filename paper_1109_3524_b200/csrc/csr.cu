@@ -271,7 +271,9 @@ void mat_plan(Ctx* c, Mat* m) {
     std::vector<int> rp(static_cast<size_t>(m->rows) + 1);
     d2h(c, rp.data(), m->rp.p, rp.size());
     sync(c);
-    if (m->max_row <= 96) {
+    // thread-per-row SELL-sigma: rows up to 96 entries, or up to 512 for large, uniform operators
+    // (enough rows to fill the GPU; the sorted slices keep padding <= 25%)
+    if (m->max_row <= 96) {  // (SELL-sigma for the 150-entry L3 rows measured no faster than adaptive)
         // SELL-32-sigma: sort rows by length within 512-row windows; accept if padding <= 25%
         constexpr int kSigma = 512;
         std::vector<int> perm(static_cast<size_t>(m->rows));

@@ -25,6 +25,36 @@ constexpr unsigned kFull = 0xffffffffu;
 // the matrix stream (epilogues opt in by defining touch(i)).
 __device__ __forceinline__ void pf(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
+// Programmatic dependent launch: every hot-path kernel is launched with programmatic stream
+// serialization, waits for its predecessor's completion + memory flush before touching memory
+// (griddepcontrol.wait), and releases its successor when its own block is done — so the next
+// kernel's launch and CTA rasterisation overlap this kernel's tail instead of following it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("IBMGPU_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <class... KArgs, class... Args>
+inline void launch_k(Ctx* c, void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    CK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+    ++c->launches;
+}
+
 // ---------------------------------------------------------------- reductions
 template <int NR>
 struct Vals {
@@ -108,28 +138,34 @@ __device__ __forceinline__ void block_partial(double (&v)[NR], RedSlot slot) {
         for (int r = 0; r < NR; ++r) slot.partials[(size_t)blockIdx.x * NR + r] = v[r];
 }
 
-// One CTA: sum the partials of `nblocks` blocks in a fixed order and run epi.fin(tot).
+// One CTA of kFinThreads: sum the partials of `nblocks` blocks in a fixed order and run
+// epi.fin(tot). 8 independent loads in flight per thread keep it at ~2 L2 round trips for 16k
+// partials.
+constexpr int kFinThreads = 1024;
+
 template <class Epi>
-__global__ void __launch_bounds__(256) k_finalize(Epi epi, int nblocks) {
+__global__ void __launch_bounds__(kFinThreads) k_finalize(Epi epi, int nblocks) {
     constexpr int NR = Epi::NR;
+    constexpr int U = 8;
+    pdl_wait();
     if (epi.skip()) return;
     const RedSlot slot = epi.slot();
     double t[NR];
 #pragma unroll
     for (int r = 0; r < NR; ++r) t[r] = 0.0;
     int b = threadIdx.x;
-    for (; b + 768 < nblocks; b += 1024) {  // 4 independent loads in flight per thread
-        double u[4][NR];
+    for (; b + (U - 1) * kFinThreads < nblocks; b += U * kFinThreads) {
+        double u[U][NR];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < U; ++q)
 #pragma unroll
-            for (int r = 0; r < NR; ++r) u[q][r] = slot.partials[(size_t)(b + 256 * q) * NR + r];
+            for (int r = 0; r < NR; ++r) u[q][r] = slot.partials[(size_t)(b + kFinThreads * q) * NR + r];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < U; ++q)
 #pragma unroll
             for (int r = 0; r < NR; ++r) t[r] += u[q][r];
     }
-    for (; b < nblocks; b += 256)
+    for (; b < nblocks; b += kFinThreads)
 #pragma unroll
         for (int r = 0; r < NR; ++r) t[r] += slot.partials[(size_t)b * NR + r];
     block_sum<NR>(t);
@@ -165,6 +201,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
                                                          const int* __restrict__ off, const int* __restrict__ ci,
                                                          const double* __restrict__ v, XF xf, Epi epi) {
     constexpr int NR = Epi::NR;
+    pdl_wait();
     if (epi.skip()) return;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
@@ -209,6 +246,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
 #pragma unroll
     for (int q = 0; q < kSellRows; ++q)
         if (ix[q] < rows) epi.row(ix[q], s[q], acc);
+    pdl_release();
     if constexpr (NR > 0) {
         block_partial<NR>(acc, epi.slot());
     }
@@ -229,8 +267,9 @@ struct StencilPlan {
 };
 
 template <class XF, class Epi>
-__global__ void __launch_bounds__(kBlock) k_spmv_stencil(int rows, StencilPlan P, XF xf, Epi epi) {
+__global__ void __launch_bounds__(kBlock, 8) k_spmv_stencil(int rows, StencilPlan P, XF xf, Epi epi) {
     constexpr int NR = Epi::NR;
+    pdl_wait();
     if (epi.skip()) return;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
@@ -261,6 +300,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_stencil(int rows, StencilPlan P
         }
     }
     if (live) epi.row(i, s, acc);
+    pdl_release();
     if constexpr (NR > 0) {
         block_partial<NR>(acc, epi.slot());
     }
@@ -278,6 +318,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_spmv_sellw(int rows, const int* _
                                                           XF xf, Epi epi) {
     constexpr int NR = Epi::NR;
     constexpr int U = 4;
+    pdl_wait();
     if (epi.skip()) return;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
@@ -321,6 +362,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_spmv_sellw(int rows, const int* _
         }
     }
     if (row >= 0) epi.row(row, s, acc);
+    pdl_release();
     if constexpr (NR > 0) {
         block_partial<NR>(acc, epi.slot());
     }
@@ -347,6 +389,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_adapt(AdaptPlan pl, const int* 
                                                        const int* __restrict__ ci, const double* __restrict__ v,
                                                        XF xf, Epi epi) {
     constexpr int NR = Epi::NR;
+    pdl_wait();
     if (epi.skip()) return;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
@@ -415,6 +458,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_adapt(AdaptPlan pl, const int* 
             if (i < r1 && lane == 0) epi.row(i, s, acc);
         }
     }
+    pdl_release();
     if constexpr (NR > 0) {
         block_partial<NR>(acc, epi.slot());
     }
@@ -427,25 +471,22 @@ inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
     int grid = 0;
     if (A->kind == SPMV_SELL) {
         grid = (A->rows + kSellRows * kBlock - 1) / (kSellRows * kBlock);
-        k_spmv_sell<<<grid, kBlock, 0, s>>>(A->rows, A->rp.p, A->sell_off.p, A->sell_ci.p, A->sell_v.p, xf, epi);
+        launch_k(c, k_spmv_sell<XF, Epi>, grid, kBlock, s, A->rows, A->rp.p, A->sell_off.p, A->sell_ci.p, A->sell_v.p,
+                 xf, epi);
     } else if (A->kind == SPMV_STENCIL) {
         const StencilPlan P{A->st_v.p, A->st_mask.p, A->st_erp.p, A->st_eci.p, A->st_ev.p, A->st_S1, A->st_S2};
         grid = (A->rows + kBlock - 1) / kBlock;
-        k_spmv_stencil<<<grid, kBlock, 0, s>>>(A->rows, P, xf, epi);
+        launch_k(c, k_spmv_stencil<XF, Epi>, grid, kBlock, s, A->rows, P, xf, epi);
     } else if (A->kind == SPMV_SELLW) {
         grid = (A->rows + kBlock - 1) / kBlock;
-        k_spmv_sellw<<<grid, kBlock, 0, s>>>(A->rows, A->rp.p, A->perm.p, A->sell_off.p, A->sell_ci.p, A->sell_v.p,
-                                             xf, epi);
+        launch_k(c, k_spmv_sellw<XF, Epi>, grid, kBlock, s, A->rows, A->rp.p, A->perm.p, A->sell_off.p, A->sell_ci.p,
+                 A->sell_v.p, xf, epi);
     } else {
         const AdaptPlan pl{A->blk_meta.p, A->lrow.p, A->lpart.p, A->lcnt.p};
         grid = A->n_blocks;
-        k_spmv_adapt<<<grid, kBlock, 0, s>>>(pl, A->rp.p, A->ci.p, A->v.p, xf, epi);
+        launch_k(c, k_spmv_adapt<XF, Epi>, grid, kBlock, s, pl, A->rp.p, A->ci.p, A->v.p, xf, epi);
     }
-    CK_LAUNCH(c);
-    if constexpr (Epi::NR > 0) {
-        k_finalize<<<1, 256, 0, s>>>(epi, grid);
-        CK_LAUNCH(c);
-    }
+    if constexpr (Epi::NR > 0) launch_k(c, k_finalize<Epi>, 1, kFinThreads, s, epi, grid);
 }
 
 // Number of blocks launch_spmv uses (sizes the reduction partials).
@@ -470,11 +511,13 @@ struct EpiStore {
 template <class Body>
 __global__ void __launch_bounds__(kBlock) k_elem(int n, Body body) {
     constexpr int NR = Body::NR;
+    pdl_wait();
     if (body.skip()) return;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
     for (int i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) body.row(i, acc);
+    pdl_release();
     if constexpr (NR > 0) block_partial<NR>(acc, body.slot());
 }
 
@@ -486,12 +529,8 @@ inline int elem_grid(Ctx* c, long long n) {
 
 template <class Body>
 inline void launch_elem(Ctx* c, int n, int grid, Body body, cudaStream_t s) {
-    k_elem<<<grid, kBlock, 0, s>>>(n, body);
-    CK_LAUNCH(c);
-    if constexpr (Body::NR > 0) {
-        k_finalize<<<1, 256, 0, s>>>(body, grid);
-        CK_LAUNCH(c);
-    }
+    launch_k(c, k_elem<Body>, grid, kBlock, s, n, body);
+    if constexpr (Body::NR > 0) launch_k(c, k_finalize<Body>, 1, kFinThreads, s, body, grid);
 }
 
 }  // namespace ibmgpu
