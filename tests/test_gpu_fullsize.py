@@ -1,0 +1,78 @@
+"""GPU parity at the benchmark sizes (C2: 1042^2, S-4M: 2040^2) against hashes produced by the
+unmodified reference (tests/golden/make_golden_large.py): bit-exact E/H/Q/lhs2, structure of
+every SA level and identical aggregates, PCG iteration counts within ±2 on the runner.hpp bench
+right-hand side, and the first time step's iterations, Cd and field norms."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_1109_3524_b200 import ibm
+from tests import helpers as H
+
+pytestmark = pytest.mark.gpu
+
+CFG = {"c2": ("cylinder_re40", 0.002, 0.001), "s4m": ("cylinder_re3000", 0.001, 2.5e-4)}
+
+
+def gold():
+    with open(os.path.join(H.GOLDEN, "hashes_large.json")) as f:
+        return json.load(f)
+
+
+@pytest.fixture(scope="module", params=["c2", "s4m"])
+def case(request):
+    name, h, dt = CFG[request.param]
+    return request.param, ibm.Stepper(H.case(name), h_min=h, dt=dt)
+
+
+def test_operators_bit_exact(case):
+    key, st = case
+    g = gold()[key]
+    assert (st.nx, st.ny, st.n_lambda) == (g["nx"], g["ny"], g["n_lambda"])
+    for k in ("G", "E", "H", "A", "BN", "Q", "QT", "lhs2"):
+        assert H.csr_hash(H.dev_to_csr(st.op(k))) == (g[k]["struct"], g[k]["values"]), k
+
+
+def test_hierarchy_structure_and_aggregates(case):
+    key, st = case
+    g = gold()[key]
+    h = st.hierarchy()
+    assert h.n_levels == len(g["levels"])
+    for l, gl in enumerate(g["levels"]):
+        lv = h.level(l)
+        for k in ("A", "P", "Pt"):
+            m = H.dev_to_csr(lv[k])
+            assert H.csr_hash(m)[0] == gl[k]["struct"], (l, k)
+            assert abs(np.sum(m.v) - gl[k]["vsum"]) <= 1e-11 * gl[k]["vabs"], (l, k)
+        assert lv["omega"] == pytest.approx(gl["omega"], rel=1e-12)
+        n_agg, agg = h.aggregates(l)
+        n_core = lv["A"].rows() - 2 * st.n_b
+        assert n_agg == gl["n_agg"]
+        assert hashlib.sha256(np.ascontiguousarray(agg[:n_core], np.int32).tobytes()).hexdigest() == gl["agg"], l
+
+
+def test_bench_solves_iteration_parity(case):
+    key, st = case
+    g = gold()[key]
+    A = st.op("lhs2")
+    b = H.bench_rhs(A.spmv, A.rows())
+    r = ibm.pcg(A, b, None, ibm.SaPreconditioner(st.hierarchy()), ibm.SolverParams())
+    assert r.converged() and abs(r.iterations - g["bench_pcg_sa"]["iterations"]) <= 2
+    rd = ibm.pcg(A, b, None, ibm.DiagonalPreconditioner(A), ibm.SolverParams())
+    assert rd.converged() and abs(rd.iterations - g["bench_pcg_diag"]["iterations"]) <= 2
+
+
+def test_first_step_matches_reference(case):
+    key, st = case
+    s0 = gold()[key]["steps"][0]
+    r = st.advance()
+    assert r.ok, r.message
+    assert abs(r.solve1_iters - s0["s1"]) <= 2 and abs(r.solve2_iters - s0["s2"]) <= 2
+    f = st.forces()
+    assert abs(f["cd"] - s0["cd"]) <= 1e-6 * abs(s0["cd"])
+    assert abs(np.linalg.norm(st.get("q")) - s0["qn"]) <= 1e-6 * s0["qn"]
+    assert abs(np.linalg.norm(st.get("lambda")) - s0["ln"]) <= 1e-6 * s0["ln"]
+    assert r.div_residual <= 10 * 1e-5 and r.noslip_residual <= 10 * 1e-5
