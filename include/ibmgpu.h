@@ -234,6 +234,51 @@ int ibmgpu_hostcase_csr(ibmgpu_hostcase_t h, const char* name, int* rows, int* c
 int ibmgpu_hostcase_move(ibmgpu_hostcase_t h, double t);
 int ibmgpu_hostcase_free(ibmgpu_hostcase_t h);
 
+/* ---------------------------------------------------------------- row-slab multi-GPU
+ * The reference is single-address-space; these entries are the distributed form of
+ * pcg (krylov.hpp:70-136) with the SaPreconditioner (amg.hpp:237-246). Every rank passes the FULL
+ * matrix and hierarchy (built identically everywhere) and the row owner of every row; each rank
+ * keeps its owned rows with halo-extended columns, fine levels distributed, levels below
+ * min_dist_rows replicated. Context with nranks > 1: NCCL between processes (ibmgpu_init with the
+ * id from ibmgpu_nccl_unique_id on rank 0). Single-rank context: virtual_ranks > 1 emulates the
+ * whole partition on this GPU (loopback halos), for parity tests of the decomposition. */
+typedef struct ibmgpu_dist* ibmgpu_dist_t;
+int ibmgpu_nccl_unique_id(void* id128);
+int ibmgpu_dist_create(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, int precond, ibmgpu_hier_t hier, const int* owner_host,
+                       int virtual_ranks, int min_dist_rows, ibmgpu_dist_t* out);
+/* info: nranks, distributed levels, loopback, own rows (first local rank), its A halo, local ranks,
+ * hierarchy levels, SpMV kind of the local A */
+int ibmgpu_dist_info(ibmgpu_dist_t d, int* info8);
+/* b_dev, x_dev: full-length device vectors on every rank; x holds x0 on entry (owned rows used) and
+ * the full solution on exit on every rank */
+int ibmgpu_dist_pcg(ibmgpu_dist_t d, const double* b_dev, double* x_dev, const ibm_solver_params* params,
+                    ibm_solve_result* result, double* history_host);
+int ibmgpu_dist_destroy(ibmgpu_dist_t d);
+/* Run the stepper's modified-Poisson solve (stepper.hpp:294-313) row-slab distributed: lambda rows
+ * by ibmgpu_partition_lambda, re-planned whenever the body operators or the hierarchy are rebuilt.
+ * Multi-rank context: all ctx ranks (virtual_ranks ignored). Single-rank context: virtual_ranks
+ * emulated ranks (0 switches back to the single-GPU graph solve). */
+int ibmgpu_stepper_distribute(ibmgpu_stepper_t st, int virtual_ranks, int min_dist_rows);
+
+/* host-only halo planning (no CUDA): rank `rank`'s part of an rows x cols CSR under row/column
+ * owners. sizes6: own rows, own input entries, halo entries, local nnz, send entries, nranks. */
+typedef struct ibmgpu_distplan* ibmgpu_distplan_t;
+int ibmgpu_distplan_build(int rows, int cols, const int* rptr, const int* cidx, const double* val,
+                          const int* row_owner, const int* col_owner, int rank, int nranks, ibmgpu_distplan_t* out);
+int ibmgpu_distplan_sizes(ibmgpu_distplan_t p, int* sizes6);
+/* any output may be NULL: rows[own rows], own[own inputs], rptr[own rows+1], cidx/val[local nnz]
+ * (extended numbering), recv_off[nranks+1], halo[halo] (global ids), send_off[nranks+1],
+ * send_idx[send entries] (owned-local indices) */
+int ibmgpu_distplan_get(ibmgpu_distplan_t p, int* rows, int* own, int* rptr, int* cidx, double* val, int* recv_off,
+                        int* halo, int* send_off, int* send_idx);
+int ibmgpu_distplan_free(ibmgpu_distplan_t p);
+/* row owners of the coupled system: pressure rows by balanced j-slabs, the two force rows of body
+ * point k by the slab of body_cell_j[k] */
+int ibmgpu_partition_lambda(int nx, int ny, int n_b, const int* body_cell_j, int nranks, int* owner);
+/* owners of level l+1 (n_agg aggregates, then the identity tail) from level l's: an aggregate
+ * goes to the owner of its lowest-index member (amg.hpp:79-107 numbering, :166-178 tail) */
+int ibmgpu_partition_coarse(int n_core, const int* agg, int n_agg, int tail, const int* owner_fine, int* owner_coarse);
+
 #ifdef __cplusplus
 }
 #endif

@@ -122,6 +122,18 @@ _SIGS = [
     ("ibmgpu_hostcase_csr", C.c_int, [_vp, C.c_char_p, _ip, _ip, _ip, _ip, _ip, _dp]),
     ("ibmgpu_hostcase_move", C.c_int, [_vp, C.c_double]),
     ("ibmgpu_hostcase_free", C.c_int, [_vp]),
+    ("ibmgpu_nccl_unique_id", C.c_int, [_vp]),
+    ("ibmgpu_dist_create", C.c_int, [_vp, _vp, C.c_int, _vp, _ip, C.c_int, C.c_int, C.POINTER(_vp)]),
+    ("ibmgpu_dist_info", C.c_int, [_vp, _ip]),
+    ("ibmgpu_dist_pcg", C.c_int, [_vp, _dp, _dp, C.POINTER(SolverParamsC), C.POINTER(SolveResultC), _dp]),
+    ("ibmgpu_dist_destroy", C.c_int, [_vp]),
+    ("ibmgpu_stepper_distribute", C.c_int, [_vp, C.c_int, C.c_int]),
+    ("ibmgpu_distplan_build", C.c_int, [C.c_int, C.c_int, _ip, _ip, _dp, _ip, _ip, C.c_int, C.c_int, C.POINTER(_vp)]),
+    ("ibmgpu_distplan_sizes", C.c_int, [_vp, _ip]),
+    ("ibmgpu_distplan_get", C.c_int, [_vp, _ip, _ip, _ip, _ip, _dp, _ip, _ip, _ip, _ip]),
+    ("ibmgpu_distplan_free", C.c_int, [_vp]),
+    ("ibmgpu_partition_lambda", C.c_int, [C.c_int, C.c_int, C.c_int, _ip, C.c_int, _ip]),
+    ("ibmgpu_partition_coarse", C.c_int, [C.c_int, _ip, C.c_int, C.c_int, _ip, _ip]),
 ]
 
 _lib = None

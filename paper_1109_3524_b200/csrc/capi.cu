@@ -3,6 +3,7 @@
 #include <cstring>
 
 #include "amg.cuh"
+#include "dist.cuh"
 #include "internal.cuh"
 #include "kern.cuh"
 #include "pcg.cuh"
@@ -60,8 +61,8 @@ int ibmgpu_init(int device, int nranks, int rank, const void* nccl_id, ibmgpu_ct
         CK(cudaDeviceGetDefaultMemPool(&pool, device));
         unsigned long long thr = ~0ull;  // keep freed blocks cached in the pool
         CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-        (void)nccl_id;
         need(nranks == 1 || nccl_id != nullptr, "init: multi-rank context needs an NCCL unique id");
+        if (nranks > 1) nccl_comm_init(c, nccl_id);
     });
     if (rc) {
         if (out) *out = nullptr;
@@ -77,6 +78,7 @@ int ibmgpu_destroy(ibmgpu_ctx_t c) {
     cudaStreamSynchronize(c->stream);
     pcg_cache_free(c);
     ctx_free_extras(c);
+    nccl_comm_free(c);
     cudaEventDestroy(c->t0);
     cudaEventDestroy(c->t1);
     cudaStreamDestroy(c->stream);
@@ -321,3 +323,46 @@ extern "C" int ibmgpu_amg_solve(ibmgpu_ctx_t c, ibmgpu_mat_t A, ibmgpu_hier_t h,
         amg_solve(c, A, h, b, x, *prm, res);
     });
 }
+
+// ---------------------------------------------------------------- row-slab multi-GPU (dist.cu)
+extern "C" {
+
+int ibmgpu_nccl_unique_id(void* id128) {
+    return guard(nullptr, [&] {
+        need(id128 != nullptr, "nccl_unique_id: null output");
+        nccl_unique_id(id128);
+    });
+}
+
+int ibmgpu_dist_create(ibmgpu_ctx_t c, ibmgpu_mat_t A, int precond, ibmgpu_hier_t hier, const int* owner,
+                       int virtual_ranks, int min_dist_rows, ibmgpu_dist_t* out) {
+    return guard(c, [&] {
+        need(A && owner && out, "dist_create: null argument");
+        need(c->nranks == 1 || virtual_ranks <= 1, "dist_create: virtual ranks need a single-rank context");
+        *out = dist_create(c, A, precond, hier, owner, virtual_ranks, min_dist_rows);
+    });
+}
+
+int ibmgpu_dist_info(ibmgpu_dist_t d, int* info8) {
+    if (!d || !info8) return IBMGPU_EINVAL;
+    dist_info(d, info8);
+    return 0;
+}
+
+int ibmgpu_dist_pcg(ibmgpu_dist_t d, const double* b_dev, double* x_dev, const ibm_solver_params* prm,
+                    ibm_solve_result* res, double* history_host) {
+    if (!d) return IBMGPU_EINVAL;
+    Ctx* c = dist_ctx(d);
+    return guard(c, [&] {
+        need(b_dev && x_dev && prm, "dist_pcg: null argument");
+        dist_solve(d, b_dev, x_dev, *prm, res, history_host);
+    });
+}
+
+int ibmgpu_dist_destroy(ibmgpu_dist_t d) {
+    if (!d) return 0;
+    Ctx* c = dist_ctx(d);
+    return guard(c, [&] { dist_destroy(d); });
+}
+
+}  // extern "C"

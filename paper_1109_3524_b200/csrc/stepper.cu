@@ -23,6 +23,8 @@
 #include <numeric>
 
 #include "amg.cuh"
+#include "dist.cuh"
+#include "host/dist_plan.hpp"
 #include "host/case.hpp"
 #include "internal.cuh"
 #include "kern.cuh"
@@ -417,8 +419,15 @@ struct ibmgpu_stepper {
     cudaEvent_t ev[8] = {};
     float phase_ms[6] = {};
 
+    // row-slab solve 2 (dist.cu): enabled by ibmgpu_stepper_distribute
+    int dist_ranks = 0, dist_min_rows = 0;
+    Dist* dist = nullptr;
+    bool dist_stale = true;
+    DBuf<double> b2, x2;
+
     ~ibmgpu_stepper() {
         if (c) cudaStreamSynchronize(c->stream);
+        dist_destroy(dist);
         if (c) {
             pcg_forget(c, A, nullptr);
             pcg_forget(c, lhs2, hier);
@@ -462,6 +471,7 @@ struct ibmgpu_stepper {
 
     // refresh_body_operators (operators.hpp:445-450) on the device
     void refresh_body_operators() {
+        dist_stale = true;
         std::vector<double> hx, hy;
         host_points(hx, hy);
         const double uni[4] = {g.uniform_region.x0, g.uniform_region.x1, g.uniform_region.y0, g.uniform_region.y1};
@@ -485,7 +495,33 @@ struct ibmgpu_stepper {
         for (Mat* m : {Q, QT, lhs2}) mat_plan(c, m);
     }
 
+    // row owners of lambda: pressure j-slabs, force rows with the slab of their point's cell
+    std::vector<int> lambda_owner(int R) const {
+        std::vector<int> cj;
+        for (const auto& b : bodies)
+            for (int p = 0; p < b.n(); ++p) {
+                const int j = (int)(std::upper_bound(g.y_faces.begin(), g.y_faces.end(), b.y[p]) - g.y_faces.begin()) - 1;
+                cj.push_back(std::clamp(j, 0, g.ny - 1));
+            }
+        return ibmhost::partition_lambda(g.nx, g.ny, n_b, cj.data(), R);
+    }
+
+    void ensure_dist() {
+        if (!dist_stale && dist) return;
+        dist_destroy(dist);
+        dist = nullptr;
+        const int R = c->nranks > 1 ? c->nranks : dist_ranks;
+        const auto own = lambda_owner(R);
+        dist = dist_create(c, lhs2, IBMGPU_PC_SA, hier, own.data(), c->nranks > 1 ? 1 : dist_ranks, dist_min_rows);
+        if (b2.n != (size_t)n_lambda) {
+            b2.alloc(c, (size_t)n_lambda);
+            x2.alloc(c, (size_t)n_lambda);
+        }
+        dist_stale = false;
+    }
+
     void rebuild_hierarchy() {
+        dist_stale = true;
         Hier* h = sa_build(c, lhs2, sa);
         if (hier) {
             pcg_forget(c, nullptr, hier);
@@ -774,16 +810,25 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
         set_err(rep, "momentum solve did not converge (rel residual " + fmt_res(r1.rel_residual) + ")");
         return;
     }
-    // stage 2
-    PcgPlan* P2 = pcg_plan(c, S->lhs2, IBMGPU_PC_SA, S->hier);
+    // stage 2 (single GPU: one graph launch; distributed: row-slab PCG, dist.cu)
+    const bool distributed = S->dist_ranks > 0 || c->nranks > 1;
+    if (distributed) S->ensure_dist();
+    PcgPlan* P2 = distributed ? nullptr : pcg_plan(c, S->lhs2, IBMGPU_PC_SA, S->hier);
+    double* b2 = distributed ? S->b2.p : P2->b.p;
+    double* lam = distributed ? S->x2.p : P2->x.p;
     const Bc2 bc2{S->bl, S->bnd.p, S->dx.p, S->dy.p};
-    launch_spmv(c, S->QT, XPlain{P1->x.p}, EpiRhs2{bc2, n_p, 0, S->ub.p, P2->b.p}, s);
-    d2d(c, P2->x.p, S->lambda.p, (size_t)S->n_lambda);
+    launch_spmv(c, S->QT, XPlain{P1->x.p}, EpiRhs2{bc2, n_p, 0, S->ub.p, b2}, s);
+    d2d(c, lam, S->lambda.p, (size_t)S->n_lambda);
     CK(cudaEventRecord(S->ev[3], s));
-    P2->run(c, S->p2, nullptr);
-    CK(cudaEventRecord(S->ev[4], s));
     ibm_solve_result r2;
-    P2->finish(c, &r2);
+    if (distributed) {
+        dist_solve(S->dist, b2, lam, S->p2, &r2, nullptr);
+        CK(cudaEventRecord(S->ev[4], s));
+    } else {
+        P2->run(c, S->p2, nullptr);
+        CK(cudaEventRecord(S->ev[4], s));
+        P2->finish(c, &r2);
+    }
     rep->solve2_iters = r2.iterations;
     rep->solve2_res = r2.rel_residual;
     if (r2.status != 0) {
@@ -792,10 +837,9 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
     }
     // stage 3: projection q = q* - B^N (Q lambda)
     if (S->bn_diagonal) {
-        launch_spmv(c, S->Q, XPlain{P2->x.p}, EpiProjectDiag{P1->x.p, S->bn_diag.p, S->q_new.p, &S->sd.p->nonfinite},
-                    s);
+        launch_spmv(c, S->Q, XPlain{lam}, EpiProjectDiag{P1->x.p, S->bn_diag.p, S->q_new.p, &S->sd.p->nonfinite}, s);
     } else {
-        launch_spmv(c, S->Q, XPlain{P2->x.p}, EpiStore{S->y.p}, s);
+        launch_spmv(c, S->Q, XPlain{lam}, EpiStore{S->y.p}, s);
         launch_spmv(c, S->BN, XPlain{S->y.p}, EpiProjectGen{P1->x.p, S->q_new.p, &S->sd.p->nonfinite}, s);
     }
     CK(cudaEventRecord(S->ev[5], s));
@@ -830,7 +874,7 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
     std::swap(S->q, S->q_new);
     std::swap(S->conv_prev, S->conv);
     S->have_conv = true;
-    d2d(c, S->lambda.p, P2->x.p, (size_t)S->n_lambda);
+    d2d(c, S->lambda.p, lam, (size_t)S->n_lambda);
     S->t = t_new;
     ++S->step;
 }
@@ -1014,6 +1058,19 @@ int ibmgpu_stepper_bodies(ibmgpu_stepper_t S, double* x, double* y, double* ubx,
             ds[k] = b.ds;
         }
     return 0;
+}
+
+int ibmgpu_stepper_distribute(ibmgpu_stepper_t S, int virtual_ranks, int min_dist_rows) {
+    return sguard(S, [&] {
+        require(virtual_ranks >= 0, "stepper_distribute: virtual_ranks must be >= 0");
+        require(S->c->nranks == 1 || virtual_ranks <= 1, "stepper_distribute: virtual ranks need a single-rank context");
+        S->dist_ranks = S->c->nranks > 1 ? S->c->nranks : virtual_ranks;
+        S->dist_min_rows = min_dist_rows;
+        S->dist_stale = true;
+        dist_destroy(S->dist);
+        S->dist = nullptr;
+        if (S->dist_ranks > 0) S->ensure_dist();
+    });
 }
 
 int ibmgpu_stepper_phase_ms(ibmgpu_stepper_t S, float* ms6) {

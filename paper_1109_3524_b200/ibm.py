@@ -34,10 +34,14 @@ class Context:
 
     _default = None
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, nranks: int = 1, rank: int = 0, nccl_id: bytes | None = None):
+        """nranks > 1: one rank of an NCCL group; nccl_id from nccl_unique_id() on rank 0 (the
+        caller broadcasts it, e.g. over torch.distributed)."""
         self.lib = load()
+        self.nranks, self.rank = nranks, rank
         h = C.c_void_p()
-        check(self.lib.ibmgpu_init(device, 1, 0, None, C.byref(h)))
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        check(self.lib.ibmgpu_init(device, nranks, rank, idbuf, C.byref(h)))
         self.h = h
 
     @classmethod
@@ -564,6 +568,11 @@ class Stepper:
                                                                     ("x", "y", "ub_x", "ub_y", "ds")]))
         return {k: v[:self.n_b] for k, v in out.items()}
 
+    def distribute(self, virtual_ranks: int = 0, min_dist_rows: int = 200000):
+        """Row-slab solve 2 (ibmgpu_stepper_distribute): over the context's NCCL ranks, or
+        `virtual_ranks` emulated ranks on this GPU (0: back to the single-GPU solve)."""
+        self.ctx.check(self.ctx.lib.ibmgpu_stepper_distribute(self.h, virtual_ranks, min_dist_rows))
+
     def phase_ms(self) -> dict:
         a = (C.c_float * 6)()
         self.ctx.check(self.ctx.lib.ibmgpu_stepper_phase_ms(self.h, a))
@@ -613,3 +622,115 @@ class HostCase:
 
     def move(self, t: float):
         self.lib.ibmgpu_hostcase_move(self.h, t)
+
+
+# ----------------------------------------------------------------------------- row-slab multi-GPU (§8(e))
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; broadcast it to the other ranks)."""
+    buf = C.create_string_buffer(128)
+    check(load().ibmgpu_nccl_unique_id(buf))
+    return buf.raw
+
+
+def partition_lambda(nx: int, ny: int, body_cell_j, nranks: int) -> np.ndarray:
+    """Row owners of the coupled system: pressure rows by balanced j-slabs, the force rows of body
+    point k by the slab containing cell row body_cell_j[k] (host only)."""
+    bj = np.ascontiguousarray(body_cell_j, np.int32)
+    out = np.zeros(nx * ny + 2 * len(bj), np.int32)
+    check(load().ibmgpu_partition_lambda(nx, ny, len(bj), _i(bj), nranks, _i(out)))
+    return out
+
+
+def partition_coarse(agg, n_core: int, n_agg: int, tail: int, owner_fine) -> np.ndarray:
+    """Owners of the next coarser level: aggregate -> owner of its lowest-index member; the
+    identity tail keeps its owners (host only)."""
+    a = np.ascontiguousarray(np.asarray(agg)[:n_core], np.int32)
+    of = np.ascontiguousarray(owner_fine, np.int32)
+    out = np.zeros(n_agg + tail, np.int32)
+    check(load().ibmgpu_partition_coarse(n_core, _i(a), n_agg, tail, _i(of), _i(out)))
+    return out
+
+
+def block_partition(n: int, nranks: int) -> np.ndarray:
+    """Contiguous balanced row blocks."""
+    return ((np.arange(n, dtype=np.int64) * nranks) // max(n, 1)).astype(np.int32)
+
+
+@dataclass
+class DistPlan:
+    """One rank's part of a CSR matrix under row/column owners (host-only halo planning)."""
+    rows: np.ndarray
+    own: np.ndarray
+    rptr: np.ndarray
+    cidx: np.ndarray
+    val: np.ndarray
+    recv_off: np.ndarray
+    halo: np.ndarray
+    send_off: np.ndarray
+    send_idx: np.ndarray
+
+    @staticmethod
+    def build(rows, cols, rptr, cidx, val, row_owner, col_owner, rank, nranks) -> "DistPlan":
+        lib = load()
+        rp, ci = np.ascontiguousarray(rptr, np.int32), np.ascontiguousarray(cidx, np.int32)
+        v = np.ascontiguousarray(val, np.float64)
+        ro, co = np.ascontiguousarray(row_owner, np.int32), np.ascontiguousarray(col_owner, np.int32)
+        h = C.c_void_p()
+        check(lib.ibmgpu_distplan_build(rows, cols, _i(rp), _i(ci), _d(v), _i(ro), _i(co), rank, nranks, C.byref(h)))
+        try:
+            sz = np.zeros(6, np.int32)
+            lib.ibmgpu_distplan_sizes(h, _i(sz))
+            nrow, nown, nhalo, nnz, nsend, R = (int(x) for x in sz)
+            out = DistPlan(np.zeros(max(nrow, 1), np.int32), np.zeros(max(nown, 1), np.int32),
+                           np.zeros(nrow + 1, np.int32), np.zeros(max(nnz, 1), np.int32), np.zeros(max(nnz, 1)),
+                           np.zeros(R + 1, np.int32), np.zeros(max(nhalo, 1), np.int32), np.zeros(R + 1, np.int32),
+                           np.zeros(max(nsend, 1), np.int32))
+            lib.ibmgpu_distplan_get(h, _i(out.rows), _i(out.own), _i(out.rptr), _i(out.cidx), _d(out.val),
+                                    _i(out.recv_off), _i(out.halo), _i(out.send_off), _i(out.send_idx))
+            out.rows, out.own, out.halo = out.rows[:nrow], out.own[:nown], out.halo[:nhalo]
+            out.cidx, out.val, out.send_idx = out.cidx[:nnz], out.val[:nnz], out.send_idx[:nsend]
+            return out
+        finally:
+            lib.ibmgpu_distplan_free(h)
+
+
+class DistSolver:
+    """Row-slab distributed PCG (ibmgpu_dist_*): the distributed form of pcg(A, b, x0, M) with M
+    identity, diagonal or SA. A and the hierarchy are the full operators; `owner` gives each row's
+    rank. With a single-rank context, `virtual_ranks` > 1 emulates the partition on this GPU."""
+
+    def __init__(self, A: SparseMatrix, M, owner, virtual_ranks: int = 1, min_dist_rows: int = 0):
+        self.ctx, self.A, self.M = A.ctx, A, M
+        own = np.ascontiguousarray(owner, np.int32)
+        if len(own) != A.rows():
+            raise ValueError("dist: owner length must equal the matrix rows")
+        h = C.c_void_p()
+        self.ctx.check(self.ctx.lib.ibmgpu_dist_create(self.ctx.h, A.h, M.kind, M.hier.h if M.hier is not None else None,
+                                                       _i(own), virtual_ranks, min_dist_rows, C.byref(h)))
+        self.h = h
+
+    def info(self) -> dict:
+        a = np.zeros(8, np.int32)
+        self.ctx.lib.ibmgpu_dist_info(self.h, _i(a))
+        keys = ("nranks", "dist_levels", "loopback", "own_rows", "halo", "local_ranks", "levels", "spmv_kind")
+        return dict(zip(keys, (int(x) for x in a)))
+
+    def solve(self, b, x0=None, params: SolverParams | None = None) -> SolveResult:
+        params = params or SolverParams()
+        params.validate()
+        n = self.A.rows()
+        bd = _as_dev(b, n, self.ctx)
+        xd = _as_dev(x0 if x0 is not None and len(x0) else None, n, self.ctx)
+        res = SolveResultC()
+        hist = np.zeros(params.max_iters + 2) if params.record_history else None
+        pc = params.c()
+        self.ctx.check(self.ctx.lib.ibmgpu_dist_pcg(self.h, bd.p, xd.p, C.byref(pc), C.byref(res),
+                                                    _d(hist) if hist is not None else None))
+        return SolveResult(x=xd.download(), iterations=res.iterations, rel_residual=res.rel_residual,
+                           status=res.status, history=list(hist[:res.history_len]) if hist is not None else [])
+
+    def __del__(self):
+        try:
+            self.ctx.lib.ibmgpu_dist_destroy(self.h)
+        except Exception:
+            pass
