@@ -424,8 +424,16 @@ struct ibmgpu_dist {
     std::vector<int> own_off;                              // R + 1
     ibmgpu::DBuf<double> gather_buf;                       // NCCL: R * max_own
     int max_own = 0;
-    long long comm_bytes = 0;                              // halo + allreduce bytes per iteration (info)
-    int halo_exchanges = 0;
+    cudaGraphExec_t iter_exec = nullptr;                   // one captured PCG iteration
+    int iter_kernels = 0;
+    int* done_host = nullptr;                              // pinned, 2 slots
+    cudaEvent_t ev[2] = {};
+    ~ibmgpu_dist() {
+        if (iter_exec) cudaGraphExecDestroy(iter_exec);
+        if (done_host) cudaFreeHost(done_host);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
 };
 
 namespace ibmgpu {
@@ -578,6 +586,60 @@ void dist_vcycle(Dist* d) {
             }
         }
     }
+}
+
+}  // namespace
+}  // namespace ibmgpu
+
+// ---------------------------------------------------------------- one PCG iteration
+namespace ibmgpu {
+namespace {
+
+void scal_all(Dist* d, int phase) {
+    for (auto& rk : d->ranks)
+        launch_k(d->c, k_dscal, 1, 1, d->c->stream, rk->st.p, (const double*)rk->red.p, phase, d->kind);
+}
+
+// krylov.hpp:104-131, every local rank; scalars stay on the device
+void enqueue_iteration(Dist* d) {
+    Ctx* c = d->c;
+    cudaStream_t s = c->stream;
+    const int kind = d->kind;
+    auto red = [](RankData& rk) { return rk.red.p; };
+    auto rslot = [](RankData& rk) { return RedSlot{rk.partials.p, nullptr}; };
+    exchange(d, [](RankData& rk) -> DMat& { return rk.A; }, [](RankData& rk) { return rk.p.p; });
+    for (auto& rk : d->ranks)
+        spmv_red(c, rk->A.m, rk->red.p, XPlain{rk->p.p}, EpiDAp{rk->p.p, rk->Ap.p, rslot(*rk), rk->red.p, rk->st.p},
+                 s);
+    allreduce(d, red, 1);
+    scal_all(d, PH_ALPHA);
+    for (auto& rk : d->ranks)
+        launch_elem(c, rk->n_own, elem_grid(c, rk->n_own),
+                    BodyDUpdate{rk->x.p, rk->r.p, rk->p.p, rk->Ap.p, rk->invd.p, rk->z.p, kind, rslot(*rk), rk->red.p,
+                                rk->st.p},
+                    s);
+    allreduce(d, red, 2);
+    scal_all(d, PH_REL);
+    if (kind == IBMGPU_PC_SA) {
+        dist_vcycle(d);
+        allreduce(d, red, 1);
+        scal_all(d, PH_BETA);
+    }
+    for (auto& rk : d->ranks)
+        if (rk->n_own) launch_elem(c, rk->n_own, elem_grid(c, rk->n_own), BodyDP{rk->z.p, rk->p.p, rk->st.p}, s);
+}
+
+void capture_iteration(Dist* d) {
+    Ctx* c = d->c;
+    const long long l0 = c->launches;
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    enqueue_iteration(d);
+    CK(cudaStreamEndCapture(c->stream, &g));
+    CK(cudaGraphInstantiate(&d->iter_exec, g, 0));
+    CK(cudaGraphDestroy(g));
+    d->iter_kernels = (int)(c->launches - l0);
+    c->launches = l0;  // capture is not execution
 }
 
 }  // namespace
@@ -736,6 +798,8 @@ Dist* dist_create(Ctx* c, Mat* A, int kind, Hier* h, const int* owner0, int virt
         CK(cudaMallocHost(&rk->host_st, sizeof(PcgState)));
         d->ranks.push_back(std::move(rk));
     }
+    CK(cudaMallocHost(&d->done_host, 2 * sizeof(int)));
+    for (auto& e : d->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     sync(c);
     return d.release();
 }
@@ -792,30 +856,35 @@ void dist_solve(Dist* d, const double* b_full, double* x_full, const ibm_solver_
         scal(PH_RZ0);
     }
     PcgState* H0 = d->ranks[0]->host_st;
-    for (;;) {
-        CK(cudaMemcpyAsync(H0, d->ranks[0]->st.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
-        sync(c);
-        if (H0->done) break;
-        exchange(d, [](RankData& rk) -> DMat& { return rk.A; }, [](RankData& rk) { return rk.p.p; });
-        for (auto& rk : d->ranks)
-            spmv_red(c, rk->A.m, rk->red.p, XPlain{rk->p.p}, EpiDAp{rk->p.p, rk->Ap.p, rslot(*rk), rk->red.p, rk->st.p},
-                     s);
-        allreduce(d, red, 1);
-        scal(PH_ALPHA);
-        for (auto& rk : d->ranks)
-            launch_elem(c, rk->n_own, elem_grid(c, rk->n_own),
-                        BodyDUpdate{rk->x.p, rk->r.p, rk->p.p, rk->Ap.p, rk->invd.p, rk->z.p, kind, rslot(*rk),
-                                    rk->red.p, rk->st.p},
-                        s);
-        allreduce(d, red, 2);
-        scal(PH_REL);
-        if (kind == IBMGPU_PC_SA) {
-            dist_vcycle(d);
-            allreduce(d, red, 1);
-            scal(PH_BETA);
+    CK(cudaMemcpyAsync(H0, d->ranks[0]->st.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    sync(c);
+    if (!H0->done) {
+        if (c->eager) {
+            // profiling mode (IBMGPU_EAGER=1): kernels launched from the host, checked every iteration
+            for (;;) {
+                enqueue_iteration(d);
+                CK(cudaMemcpyAsync(H0, d->ranks[0]->st.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+                sync(c);
+                if (H0->done) break;
+            }
+        } else {
+            // one graph launch per iteration (NCCL calls captured with the kernels); the done flag
+            // of iteration k is read while iteration k+1 is already queued, so the GPU never idles
+            // on the host check — the extra iteration's kernels see `done` and exit at once
+            if (!d->iter_exec) capture_iteration(d);
+            const int* done_dev = &d->ranks[0]->st.p->done;
+            for (int k = 0;; ++k) {
+                CK(cudaGraphLaunch(d->iter_exec, s));
+                c->launches += d->iter_kernels;
+                CK(cudaMemcpyAsync(d->done_host + (k & 1), done_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
+                CK(cudaEventRecord(d->ev[k & 1], s));
+                if (k > 0) {
+                    CK(cudaEventSynchronize(d->ev[(k - 1) & 1]));
+                    if (d->done_host[(k - 1) & 1]) break;
+                }
+                require(k <= prm.max_iters + 2, "dist: iteration loop did not terminate");
+            }
         }
-        for (auto& rk : d->ranks)
-            if (rk->n_own) launch_elem(c, rk->n_own, elem_grid(c, rk->n_own), BodyDP{rk->z.p, rk->p.p, rk->st.p}, s);
     }
     // x (owned rows) back into the full vector on every rank
     if (d->loop) {
@@ -828,6 +897,7 @@ void dist_solve(Dist* d, const double* b_full, double* x_full, const ibm_solver_
         if (rk.n_own) launch_elem(c, rk.n_own, elem_grid(c, rk.n_own), BodyScatter{rk.own0_dev.p, rk.x.p, x_full}, s);
         NK(nccl_api().allReduce(x_full, x_full, (size_t)d->n, ncclDouble, ncclSum, static_cast<ncclComm_t>(c->nccl), s));
     }
+    CK(cudaMemcpyAsync(H0, d->ranks[0]->st.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
     sync(c);
     if (res) {
         res->iterations = H0->iterations;

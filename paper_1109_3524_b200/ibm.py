@@ -77,6 +77,9 @@ def _ctx(ctx):
 class DeviceVector:
     """A device array of doubles (ibmgpu_vec_alloc)."""
 
+    def __len__(self):
+        return self.n
+
     def __init__(self, n: int, ctx: Context | None = None):
         self.ctx = _ctx(ctx)
         self.n = int(n)

@@ -1,0 +1,86 @@
+"""Cost of the row-slab decomposition on one GPU (csrc/dist.cu, loopback communicator).
+
+For a workload's coupled system (bench_rhs of runner.hpp) it times, on the device:
+  single   ibmgpu_pcg (one conditional-graph launch)
+  dist R   ibmgpu_dist_pcg with R emulated ranks (one graph launch per iteration, halos by D2D copy)
+Loopback runs every rank's kernels back to back on this GPU, so time/R approximates one rank's
+compute share when the R slabs run on R GPUs (communication not included). Prints JSON.
+
+  python tools/dist_bench.py [--workload c2|s4m|c5-N] [--ranks 1,2,4,8] [--min-dist-rows 200000]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from bench import CASES, workload  # noqa: E402
+from paper_1109_3524_b200 import ibm  # noqa: E402
+
+
+def cell_j(y_faces, y):
+    return np.clip(np.searchsorted(y_faces, y, side="right") - 1, 0, len(y_faces) - 2).astype(np.int32)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--ranks", default="1,2,4,8")
+    ap.add_argument("--min-dist-rows", type=int, default=200000)
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    cfg, h_min, dt, desc = workload(a.workload)
+    st = ibm.Stepper(os.path.join(CASES, cfg + ".cfg"), h_min=h_min, dt=dt)
+    ctx = st.ctx
+    A = st.op("lhs2")
+    n = A.rows()
+    w = np.sin(0.7 * np.arange(n) + 0.3)
+    w[0] = 0.0
+    w /= np.linalg.norm(w)
+    b = A.spmv(w)
+    M = ibm.SaPreconditioner(st.hierarchy())
+    bd = ibm.DeviceVector.from_host(b, ctx)
+    out = {"workload": a.workload, "desc": desc, "n": n, "results": []}
+
+    def timed(fn):
+        fn()
+        best = 1e30
+        res = None
+        for _ in range(a.reps):
+            ctx.sync()
+            ctx.timer_start()
+            res = fn()
+            best = min(best, ctx.timer_stop())
+        return best, res
+
+    def single():
+        return ibm.pcg(A, bd, None, M, ibm.SolverParams())
+
+    ms, r = timed(single)
+    out["results"].append({"mode": "single", "ms": round(ms, 3), "iters": r.iterations,
+                           "ms_per_iter": round(ms / r.iterations, 4)})
+    yf, by = st.grid()["y_faces"], st.bodies()["y"]
+    for R in (int(x) for x in a.ranks.split(",")):
+        owner = ibm.partition_lambda(st.nx, st.ny, cell_j(yf, by), R)
+        t0 = time.time()
+        ds = ibm.DistSolver(A, M, owner, virtual_ranks=R, min_dist_rows=a.min_dist_rows)
+        setup = time.time() - t0
+        ms, r = timed(lambda: ds.solve(bd))
+        info = ds.info()
+        out["results"].append({"mode": f"loopback R={R}", "ms": round(ms, 3), "iters": r.iterations,
+                               "ms_per_iter": round(ms / r.iterations, 4),
+                               "per_rank_ms_per_iter": round(ms / r.iterations / R, 4),
+                               "dist_levels": info["dist_levels"], "levels": info["levels"],
+                               "rank0_own": info["own_rows"], "rank0_halo": info["halo"],
+                               "setup_s": round(setup, 2)})
+        del ds
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
