@@ -121,6 +121,16 @@ def hier_bytes(h) -> tuple[float, dict]:
     return float(b), dict(levels=levels, n_c=nc)
 
 
+def load_traffic(workload: str):
+    """Measured DRAM bytes per solve-2 iteration from the committed ncu launch list
+    (profiles/r01/traffic.json, tools/traffic_per_iteration.py); None if not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -209,6 +219,7 @@ def run_ours(args, rank: int, world: int):
     s2_ms = sum(solve2_ms) / K
     s2_bytes = sum(its2) / K * b_it2 + spmv_bytes(st.n_lambda, st.n_lambda, st.nnz_lhs2)
     peak, peak_kind = load_peaks()
+    tr = load_traffic(args.workload)
     achieved = s2_bytes / (s2_ms * 1e-3) / 1e9
     b_step = sum(its1) / K * b_it1 + sum(its2) / K * b_it2 + b_fixed
     n_b = st.n_b
@@ -244,7 +255,10 @@ def run_ours(args, rank: int, world: int):
         "roofline": {"kernel": "solve-2 SA-PCG graph launch (SpMV + V-cycle + fused reductions)",
                      "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "frac_of_8tbs": round(achieved / 8000, 4),
-                     "bytes_per_launch": s2_bytes, "b_it2": b_it2, "traffic": None},
+                     "bytes_per_launch": s2_bytes, "b_it2": b_it2,
+                     "traffic": (round(sum(its2) / K * tr["dram_bytes_per_iteration"]) if tr else None),
+                     "traffic_per_iteration": tr["dram_bytes_per_iteration"] if tr else None,
+                     "traffic_source": tr["source"] if tr else None},
         "e2e": {"value": round(K / e2e_s * (1 if slab else world), 4), "unit": "steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,

@@ -353,6 +353,9 @@ void plan_adaptive_from(Ctx* c, Mat* m, const std::vector<int>& rp) {
             while (tpr < 32 && tpr * 4 < mean) tpr *= 2;
             // keep at least a few rows per group for short-row chunks
             while (tpr > 2 && (r1 - r) > (kBlock / tpr) * 8) tpr /= 2;
+            // whole passes only: a chunk of 17 rows on 8 groups costs 3 latency-bound passes, 16 cost 2
+            const int ngrp = kBlock / tpr;
+            if (r1 - r > ngrp && (r1 - r) % ngrp) r1 = r + ((r1 - r) / ngrp) * ngrp;
             meta.push_back(make_int4(r, r1, tpr, 0));
             r = r1;
         }
