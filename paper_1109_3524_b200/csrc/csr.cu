@@ -271,40 +271,63 @@ void mat_plan(Ctx* c, Mat* m) {
     std::vector<int> rp(static_cast<size_t>(m->rows) + 1);
     d2h(c, rp.data(), m->rp.p, rp.size());
     sync(c);
-    // thread-per-row SELL-sigma: rows up to 96 entries, or up to 512 for large, uniform operators
-    // (enough rows to fill the GPU; the sorted slices keep padding <= 25%)
-    if (m->max_row <= 96) {  // (SELL-sigma for the 150-entry L3 rows measured no faster than adaptive)
-        // SELL-32-sigma: sort rows by length within 512-row windows; accept if padding <= 25%
-        constexpr int kSigma = 512;
-        std::vector<int> perm(static_cast<size_t>(m->rows));
-        for (int w0 = 0; w0 < m->rows; w0 += kSigma) {
-            const int w1 = std::min(m->rows, w0 + kSigma);
-            for (int i = w0; i < w1; ++i) perm[i] = i;
-            std::stable_sort(perm.begin() + w0, perm.begin() + w1,
-                             [&](int a, int b) { return rp[a + 1] - rp[a] > rp[b + 1] - rp[b]; });
+    // thread-per-row SELL-sigma for the rows of <= 96 entries; the few longer rows (the body
+    // tail of the Galerkin levels: force unknowns couple to many aggregates) get a warp each with
+    // an in-order sum, so one long row no longer sends the whole level to the adaptive kernel
+    {
+        constexpr int kSigma = 512, kWide = 96;
+        std::vector<int> shortrows, longrows;
+        long long long_nnz = 0;
+        for (int i = 0; i < m->rows; ++i) {
+            const int l = rp[i + 1] - rp[i];
+            if (l <= kWide) {
+                shortrows.push_back(i);
+            } else {
+                longrows.push_back(i);
+                long_nnz += l;
+            }
         }
-        std::vector<int> off(static_cast<size_t>(n_slices) + 1, 0);
-        long long total = 0;
-        for (int s = 0; s < n_slices; ++s) {
-            int w = 0;
-            for (int i = s * 32; i < std::min(m->rows, s * 32 + 32); ++i) w = std::max(w, rp[perm[i] + 1] - rp[perm[i]]);
-            total += 32ll * w;
-            off[s + 1] = static_cast<int>(total);
-        }
-        if (total <= (long long)(1.25 * m->nnz) + 32 * 64 && total < (1ll << 31)) {
-            m->kind = SPMV_SELLW;
-            m->perm.alloc(c, perm.size());
-            h2d(c, m->perm.p, perm.data(), perm.size());
-            m->sell_off.alloc(c, off.size());
-            h2d(c, m->sell_off.p, off.data(), off.size());
-            m->sell_ci.alloc(c, (size_t)total);
-            m->sell_v.alloc(c, (size_t)total);
-            k_sell_fill<<<(n_slices * 32 + 255) / 256, 256, 0, c->stream>>>(m->rows, m->rp.p, m->ci.p, m->v.p,
-                                                                            m->sell_off.p, m->perm.p, m->sell_ci.p,
-                                                                            m->sell_v.p);
-            CK_LAUNCH(c);
-            sync(c);
-            return;
+        const int ns = static_cast<int>(shortrows.size());
+        // (every row > 96 on its own warp — i.e. no CSR-adaptive at all — measured 1.69 vs 1.01 ms
+        // per S-4M iteration: the in-order add chain is too long for the 150-2000-entry coarse rows)
+        const bool few_long = longrows.size() * 20 <= (size_t)m->rows && long_nnz * 3 <= (long long)m->nnz;
+        // (SELL-sigma for the 150-entry S-4M level-3 rows measured no faster than adaptive)
+        if (few_long && ns > 0) {
+            // SELL-32-sigma: sort short rows by length within 512-slot windows; accept if padding <= 25%
+            std::vector<int> perm(shortrows);
+            for (int w0 = 0; w0 < ns; w0 += kSigma) {
+                const int w1 = std::min(ns, w0 + kSigma);
+                std::stable_sort(perm.begin() + w0, perm.begin() + w1,
+                                 [&](int a, int b) { return rp[a + 1] - rp[a] > rp[b + 1] - rp[b]; });
+            }
+            const int ss = (ns + 31) / 32;
+            std::vector<int> off(static_cast<size_t>(ss) + 1, 0);
+            long long total = 0;
+            for (int sl = 0; sl < ss; ++sl) {
+                int w = 0;
+                for (int i = sl * 32; i < std::min(ns, sl * 32 + 32); ++i)
+                    w = std::max(w, rp[perm[i] + 1] - rp[perm[i]]);
+                total += 32ll * w;
+                off[sl + 1] = static_cast<int>(total);
+            }
+            if (total <= (long long)(1.25 * (m->nnz - long_nnz)) + 32 * 64 && total < (1ll << 31)) {
+                m->kind = SPMV_SELLW;
+                m->n_short = ns;
+                m->n_long = static_cast<int>(longrows.size());
+                m->perm.alloc(c, perm.size());
+                h2d(c, m->perm.p, perm.data(), perm.size());
+                m->long_rows.alloc(c, std::max<size_t>(longrows.size(), 1));
+                h2d(c, m->long_rows.p, longrows.data(), longrows.size());
+                m->sell_off.alloc(c, off.size());
+                h2d(c, m->sell_off.p, off.data(), off.size());
+                m->sell_ci.alloc(c, (size_t)std::max(total, 1ll));
+                m->sell_v.alloc(c, (size_t)std::max(total, 1ll));
+                k_sell_fill<<<(ss * 32 + 255) / 256, 256, 0, c->stream>>>(ns, m->rp.p, m->ci.p, m->v.p, m->sell_off.p,
+                                                                          m->perm.p, m->sell_ci.p, m->sell_v.p);
+                CK_LAUNCH(c);
+                sync(c);
+                return;
+            }
         }
     }
     m->kind = SPMV_VECTOR;

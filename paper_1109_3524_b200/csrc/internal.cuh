@@ -132,6 +132,9 @@ struct ibmgpu_mat {
     ibmgpu::DBuf<int> sell_ci;
     ibmgpu::DBuf<double> sell_v;
     ibmgpu::DBuf<int> perm;              // SELL-sigma: slot -> original row
+    int n_short = 0;                     // SELL-sigma slots (rows <= 96 entries)
+    int n_long = 0;                      // rows > 96 entries: one warp each, in-order sum
+    ibmgpu::DBuf<int> long_rows;
     // stencil (DIA-hybrid) plan: 5-point band {i-S, i-1, i, i+1, i+S} as 5 value planes + a
     // per-row presence mask (bit 6 selects the second stride), extras (columns > i+S, or whole
     // rows that do not fit the band) in a CSR tail — summation order equals CSR column order

@@ -311,11 +311,39 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_stencil(int rows, StencilPla
 // original row perm[i]. Entries keep their column order, so the sum is still bit-exact with
 // spmv_into. The entry loop is software-pipelined: chunk k+1's indices/values are in flight while
 // chunk k's x-gathers are consumed.
+// Rows longer than 96 entries (listed in long_rows) are handled by the CTAs after the first
+// `sblocks`, one warp per row: lanes form the products of 32 consecutive entries in parallel
+// (the next 32 already in flight) and every lane adds them in column order from shuffles —
+// the same rounding sequence as the thread-per-row sum.
+template <class XF>
+__device__ __forceinline__ double row_sum_inorder(int row, const int* __restrict__ rp, const int* __restrict__ ci,
+                                                  const double* __restrict__ v, XF xf, int lane) {
+    const int b = __ldg(rp + row), e = __ldg(rp + row + 1);
+    double s = 0.0;
+    int k = b + lane;
+    double p = k < e ? mul(__ldg(v + k), xf(__ldg(ci + k))) : 0.0;
+    for (int k0 = b; k0 < e; k0 += 32) {
+        const int kn = k0 + 32 + lane;
+        const double pn = kn < e ? mul(__ldg(v + kn), xf(__ldg(ci + kn))) : 0.0;
+        const int cnt = min(32, e - k0);
+        if (cnt == 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) s = addd(s, __shfl_sync(kFull, p, j));
+        } else {
+            for (int j = 0; j < cnt; ++j) s = addd(s, __shfl_sync(kFull, p, j));
+        }
+        p = pn;
+    }
+    return s;
+}
+
 template <class XF, class Epi>
 __global__ void __launch_bounds__(kBlock, 4) k_spmv_sellw(int rows, const int* __restrict__ rp,
                                                           const int* __restrict__ perm, const int* __restrict__ off,
                                                           const int* __restrict__ ci, const double* __restrict__ v,
-                                                          XF xf, Epi epi) {
+                                                          XF xf, Epi epi, int sblocks, const int* __restrict__ long_rows,
+                                                          int n_long, const int* __restrict__ csr_ci,
+                                                          const double* __restrict__ csr_v) {
     constexpr int NR = Epi::NR;
     constexpr int U = 4;
     pdl_wait();
@@ -323,6 +351,18 @@ __global__ void __launch_bounds__(kBlock, 4) k_spmv_sellw(int rows, const int* _
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
+    if (blockIdx.x >= sblocks) {
+        const int w = (blockIdx.x - sblocks) * (kBlock / 32) + (threadIdx.x >> 5);
+        const int lane = threadIdx.x & 31;
+        if (w < n_long) {
+            const int row = __ldg(long_rows + w);
+            const double s = row_sum_inorder(row, rp, csr_ci, csr_v, xf, lane);  // CSR arrays, not the slices
+            if (lane == 0) epi.row(row, s, acc);
+        }
+        pdl_release();
+        if constexpr (NR > 0) block_partial<NR>(acc, epi.slot());
+        return;
+    }
     const int i = blockIdx.x * kBlock + threadIdx.x;
     const int sl = i >> 5;
     const bool in_slice = sl < ((rows + 31) >> 5);
@@ -478,9 +518,11 @@ inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
         grid = (A->rows + kBlock - 1) / kBlock;
         launch_k(c, k_spmv_stencil<XF, Epi>, grid, kBlock, s, A->rows, P, xf, epi);
     } else if (A->kind == SPMV_SELLW) {
-        grid = (A->rows + kBlock - 1) / kBlock;
-        launch_k(c, k_spmv_sellw<XF, Epi>, grid, kBlock, s, A->rows, A->rp.p, A->perm.p, A->sell_off.p, A->sell_ci.p,
-                 A->sell_v.p, xf, epi);
+        const int sb = (A->n_short + kBlock - 1) / kBlock;
+        grid = sb + (A->n_long + kBlock / 32 - 1) / (kBlock / 32);
+        launch_k(c, k_spmv_sellw<XF, Epi>, grid, kBlock, s, A->n_short, A->rp.p, A->perm.p, A->sell_off.p,
+                 A->sell_ci.p, A->sell_v.p, xf, epi, sb, (const int*)A->long_rows.p, A->n_long, (const int*)A->ci.p,
+                 (const double*)A->v.p);
     } else {
         const AdaptPlan pl{A->blk_meta.p, A->lrow.p, A->lpart.p, A->lcnt.p};
         grid = A->n_blocks;
@@ -493,7 +535,9 @@ inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
 inline int spmv_grid(const Mat* A) {
     if (A->rows == 0) return 0;
     if (A->kind == SPMV_SELL) return (A->rows + kSellRows * kBlock - 1) / (kSellRows * kBlock);
-    if (A->kind == SPMV_SELLW || A->kind == SPMV_STENCIL) return (A->rows + kBlock - 1) / kBlock;
+    if (A->kind == SPMV_SELLW)
+        return (A->n_short + kBlock - 1) / kBlock + (A->n_long + kBlock / 32 - 1) / (kBlock / 32);
+    if (A->kind == SPMV_STENCIL) return (A->rows + kBlock - 1) / kBlock;
     return A->n_blocks;
 }
 

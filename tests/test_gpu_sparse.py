@@ -33,6 +33,26 @@ def test_spmv_bitwise(port):
             assert np.max(np.abs(y - yo)) <= 1e-14 * np.max(np.abs(m.v)) * np.sum(np.abs(x))
 
 
+@pytest.mark.parametrize("n_long", [1, 7, 40])
+def test_spmv_hybrid_long_rows_bitwise(port, n_long):
+    """SELL-32-sigma with a few rows of > 96 entries (the Galerkin body tail): the long rows run
+    one warp each with an in-order sum, so the whole product stays bit-exact with spmv_into."""
+    rng = np.random.default_rng(11 + n_long)
+    n = 1200
+    rows, cols, vals = [], [], []
+    long_ids = set(rng.choice(n, n_long, replace=False).tolist())
+    for i in range(n):
+        k = int(rng.integers(150, 400)) if i in long_ids else int(rng.integers(1, 30))
+        c = np.sort(rng.choice(n, size=k, replace=False))
+        rows += [i] * k
+        cols += c.tolist()
+        vals += rng.uniform(-1, 1, k).tolist()
+    m = port.from_triplets(n, n, np.array(rows), np.array(cols), np.array(vals))
+    x = rng.uniform(-1, 1, n)
+    for xv in (x, np.sin(np.arange(n) * 0.37 + 0.1)):
+        assert np.array_equal(dev(m).spmv(xv), port.spmv(m, xv))
+
+
 def test_spmv_known_answers():
     A = ibm.SparseMatrix.from_triplets(2, 2, [(0, 0, 2.0), (1, 0, 1.0), (1, 1, 3.0)])
     assert np.array_equal(A.spmv(np.ones(2)), [2.0, 4.0])
