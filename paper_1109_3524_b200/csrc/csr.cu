@@ -292,7 +292,10 @@ void mat_plan(Ctx* c, Mat* m) {
         // per S-4M iteration: the in-order add chain is too long for the 150-2000-entry coarse rows)
         const bool few_long = longrows.size() * 20 <= (size_t)m->rows && long_nnz * 3 <= (long long)m->nnz;
         // (SELL-sigma for the 150-entry S-4M level-3 rows measured no faster than adaptive)
-        if (few_long && ns > 0) {
+        // thread per row needs rows to fill the machine: a 22k-row, 33-entry level (C2 L3 P) has
+        // 7% of the thread slots busy and ran 19 us as SELL-sigma vs 14 us on the adaptive kernel
+        const bool enough_rows = m->rows >= 65536 || avg <= 8.0;
+        if (few_long && ns > 0 && enough_rows) {
             // SELL-32-sigma: sort short rows by length within 512-slot windows; accept if padding <= 25%
             std::vector<int> perm(shortrows);
             for (int w0 = 0; w0 < ns; w0 += kSigma) {

@@ -42,7 +42,7 @@ def test_spmv_hybrid_long_rows_bitwise(port, n_long):
     rows, cols, vals = [], [], []
     long_ids = set(rng.choice(n, n_long, replace=False).tolist())
     for i in range(n):
-        k = int(rng.integers(150, 400)) if i in long_ids else int(rng.integers(1, 30))
+        k = int(rng.integers(97, 160)) if i in long_ids else int(rng.integers(10, 40))
         c = np.sort(rng.choice(n, size=k, replace=False))
         rows += [i] * k
         cols += c.tolist()
