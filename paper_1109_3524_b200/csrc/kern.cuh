@@ -480,19 +480,21 @@ __global__ void __launch_bounds__(kBlock) k_spmv_adapt(AdaptPlan pl, const int* 
             double s = 0.0;
             if (i < r1) {
                 const int e = __ldg(rp + i + 1);
-                int k = __ldg(rp + i) + lane;
-                for (; k + 3 * tpr < e; k += 4 * tpr) {
+                // predicated 4-wide batches: a lane's last (partial) batch issues all its loads at
+                // once instead of one dependent index->gather chain per remaining entry
+                for (int k = __ldg(rp + i) + lane; k < e; k += 4 * tpr) {
                     int c[4];
                     double a[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        c[u] = __ldg(ci + k + u * tpr);
-                        a[u] = __ldg(v + k + u * tpr);
-                    }
+                    for (int u = 0; u < 4; ++u)
+                        if (k + u * tpr < e) {
+                            c[u] = __ldg(ci + k + u * tpr);
+                            a[u] = __ldg(v + k + u * tpr);
+                        }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) s = addd(s, mul(a[u], xf(c[u])));
+                    for (int u = 0; u < 4; ++u)
+                        if (k + u * tpr < e) s = addd(s, mul(a[u], xf(c[u])));
                 }
-                for (; k < e; k += tpr) s = addd(s, mul(__ldg(v + k), xf(__ldg(ci + k))));
             }
             for (int o = tpr >> 1; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o, tpr);
             if (i < r1 && lane == 0) epi.row(i, s, acc);
