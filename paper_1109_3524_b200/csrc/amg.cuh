@@ -31,6 +31,7 @@ struct Level {
     DBuf<double> invd, wd;  // 1/diag(A), omega/diag(A)
     DBuf<int> agg;          // aggregate id per core row
     DBuf<double> b, x, r, xo;  // V-cycle work vectors (b unused at level 0)
+    DBuf<double> xj;           // levels >= 1: (omega d) .* b, written by the restriction above
     ~Level() {
         delete A;
         delete P;
@@ -111,6 +112,22 @@ struct EpiStoreSkip {  // K2: b_{l+1} = s
     __device__ void fin(double*) const {}
 };
 
+struct EpiStoreJacobi {  // K2 into level l+1: b_i = s and the pre-smoothed iterate xj_i = (w d)_i b_i
+    static constexpr int NR = 0;
+    double* y;
+    const double* wd;
+    double* xj;
+    const int* done;
+    __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ void touch(int i) const { pf(wd + i); }
+    __device__ void row(int i, double s, double*) const {
+        y[i] = s;
+        xj[i] = mul(wd[i], s);
+    }
+    __device__ RedSlot slot() const { return {}; }
+    __device__ void fin(double*) const {}
+};
+
 struct EpiAddInPlace {  // K3: x_i += s
     static constexpr int NR = 0;
     double* x;
@@ -179,9 +196,18 @@ inline void vcycle_launch(Ctx* c, Hier* h, const double* r_in, double* z_out, co
     for (int l = 0; l < F; ++l) {
         Level& lv = *h->levels[l];
         const double* b = l == 0 ? r_in : lv.b.p;
-        launch_spmv(c, lv.A, XJacobi{lv.wd.p, b}, EpiJacobiResidual{lv.wd.p, b, lv.x.p, lv.r.p, done}, s);
-        double* bn = l + 1 < L ? h->levels[l + 1]->b.p : h->cb.p;
-        launch_spmv(c, lv.Pt, XPlain{lv.r.p}, EpiStoreSkip{bn, done}, s);
+        // level 0 forms x_j = (w d)_j r_j inside the gather; deeper levels gather the iterate the
+        // restriction above already wrote (one gather per entry instead of two)
+        if (l == 0)
+            launch_spmv(c, lv.A, XJacobi{lv.wd.p, b}, EpiJacobiResidual{lv.wd.p, b, lv.x.p, lv.r.p, done}, s);
+        else
+            launch_spmv(c, lv.A, XPlain{lv.xj.p}, EpiJacobiResidual{lv.wd.p, b, lv.x.p, lv.r.p, done}, s);
+        if (l + 1 < L) {
+            Level& nx = *h->levels[l + 1];
+            launch_spmv(c, lv.Pt, XPlain{lv.r.p}, EpiStoreJacobi{nx.b.p, nx.wd.p, nx.xj.p, done}, s);
+        } else {
+            launch_spmv(c, lv.Pt, XPlain{lv.r.p}, EpiStoreSkip{h->cb.p, done}, s);
+        }
     }
     if (F < L) {
         k_coarse_cycle<<<h->coarse_grid, kBlock, 0, s>>>(CoarsePlan{h->phases.p, h->n_phases, h->bar.p, h->bar.p + 1},

@@ -499,7 +499,7 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
             for (Mat* m : {lv.A, lv.P, lv.Pt})
                 if (!m->planned) mat_plan(c, m);
             const size_t n = (size_t)lv.A->rows;
-            if (l > 0) lv.b.alloc(c, n);
+            if (l > 0) lv.b.alloc(c, n), lv.xj.alloc(c, n);
             lv.x.alloc(c, n);
             lv.r.alloc(c, n);
             lv.xo.alloc(c, n);

@@ -506,9 +506,16 @@ void vcycle_from(Ctx* c, Hier* h, int D, const double* b_in, double* out, const 
     for (int l = D; l < L; ++l) {
         Level& lv = *h->levels[l];
         const double* b = l == D ? b_in : lv.b.p;
-        launch_spmv(c, lv.A, XJacobi{lv.wd.p, b}, EpiJacobiResidual{lv.wd.p, b, lv.x.p, lv.r.p, done}, s);
-        double* bn = l + 1 < L ? h->levels[l + 1]->b.p : h->cb.p;
-        launch_spmv(c, lv.Pt, XPlain{lv.r.p}, EpiStoreSkip{bn, done}, s);
+        if (l == D)
+            launch_spmv(c, lv.A, XJacobi{lv.wd.p, b}, EpiJacobiResidual{lv.wd.p, b, lv.x.p, lv.r.p, done}, s);
+        else
+            launch_spmv(c, lv.A, XPlain{lv.xj.p}, EpiJacobiResidual{lv.wd.p, b, lv.x.p, lv.r.p, done}, s);
+        if (l + 1 < L) {
+            Level& nx = *h->levels[l + 1];
+            launch_spmv(c, lv.Pt, XPlain{lv.r.p}, EpiStoreJacobi{nx.b.p, nx.wd.p, nx.xj.p, done}, s);
+        } else {
+            launch_spmv(c, lv.Pt, XPlain{lv.r.p}, EpiStoreSkip{h->cb.p, done}, s);
+        }
     }
     coarse_solve(c, h, h->cb.p, h->cx.p, done, s);
     for (int l = L - 1; l >= D; --l) {
