@@ -234,6 +234,7 @@ __global__ void k_pack_tiles(int n, const double* __restrict__ full, double* __r
 __global__ void __launch_bounds__(256) k_symv_tiles(int n, int nt, const double* __restrict__ tiles,
                                                     const double* __restrict__ x, double* __restrict__ prow,
                                                     double* __restrict__ pcol, const int* done) {
+    pdl_wait();
     if (done && *(volatile const int*)done) return;
     __shared__ double A[TS][TS + 1];
     __shared__ double xi[TS], xj[TS];
@@ -261,11 +262,13 @@ __global__ void __launch_bounds__(256) k_symv_tiles(int n, int nt, const double*
         for (int k = 0; k < TS; ++k) s += A[k][cc] * xi[k];
         pcol[(size_t)t * TS + cc] = s;
     }
+    pdl_release();
 }
 
 // y_I = sum_{J<=I} prow[(I,J)] + sum_{K>I} pcol[(K,I)], fixed order
 __global__ void k_symv_combine(int n, int nt, const double* __restrict__ prow, const double* __restrict__ pcol,
                                double* __restrict__ y, const int* done) {
+    pdl_wait();
     if (done && *(volatile const int*)done) return;
     const int I = blockIdx.x, r = threadIdx.x;
     if (r >= TS) return;
@@ -274,6 +277,7 @@ __global__ void k_symv_combine(int n, int nt, const double* __restrict__ prow, c
     for (int K = I + 1; K < nt; ++K) s += pcol[((size_t)K * (K + 1) / 2 + I) * TS + r];
     const int gi = I * TS + r;
     if (gi < n) y[gi] = s;
+    pdl_release();
 }
 
 }  // namespace
@@ -300,10 +304,8 @@ void launch_symv_packed(Ctx* c, int n, const double* tiles, const double* x, dou
     const int nt = (n + TS - 1) / TS;
     const int ntiles = nt * (nt + 1) / 2;
     if (ntiles == 0) return;
-    k_symv_tiles<<<ntiles, 256, 0, s>>>(n, nt, tiles, x, prow, pcol, done);
-    CK_LAUNCH(c);
-    k_symv_combine<<<nt, TS, 0, s>>>(n, nt, prow, pcol, y, done);
-    CK_LAUNCH(c);
+    launch_k(c, k_symv_tiles, ntiles, 256, s, n, nt, tiles, x, prow, pcol, done);
+    launch_k(c, k_symv_combine, nt, TS, s, n, nt, (const double*)prow, (const double*)pcol, y, done);
 }
 
 void dense_spd_inverse(Ctx* c, const Mat* Ac, double* inv) {
