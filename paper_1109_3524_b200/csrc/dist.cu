@@ -9,10 +9,12 @@
 // the rank-partial restriction P^T r is summed across ranks (one allreduce of the level-D vector),
 // and every rank runs the remaining V-cycle on full vectors (amg.cuh kernels unchanged).
 //
-// Per PCG iteration (SA): 1 + 4 D halo exchanges, 1 vector allreduce at the level switch, and 3
-// scalar allreduces (p.Ap, {r.r, r.z}, r.z). Because every local matrix keeps the global entry
-// order inside a row, every distributed SpMV rounds exactly like the single-GPU one; only the dot
-// products (sums of per-rank partials) and the switch restriction differ in rounding.
+// Per PCG iteration (SA): 1 + 4 D halo exchanges, 1 vector allreduce at the level switch, and ONE
+// scalar allreduce: the single-reduction recurrence applies the SpMV to z
+// (w = A z) and reduces {r.r, r.z, z.w, z.Ap_old} together; A p follows as w + beta Ap_old and
+// p.Ap from the recurrence. Because every local matrix keeps the global entry order inside a row,
+// every distributed SpMV rounds exactly like the single-GPU one; the dot products (sums of
+// per-rank partials), the recurrence for p.Ap and the switch restriction differ in rounding.
 //
 // Communication backends: NCCL (one process per GPU; grouped ncclSend/ncclRecv for halos,
 // ncclAllReduce for scalars and the switch vector), or loopback — all ranks of the partition
@@ -178,113 +180,83 @@ struct BodyDZeroX {
     __device__ void fin(double*) const {}
 };
 
-struct BodyDInitZ {  // z = M r (identity / diagonal), p = z ; partial r.z
-    static constexpr int NR = 1;
+struct BodyDPrecond {  // z = M r for the identity / diagonal preconditioners (krylov.hpp:46-66)
+    static constexpr int NR = 0;
     const double* r;
     const double* invd;
     double* z;
-    double* p;
-    RedSlot rs;
-    double* red;
     const PcgState* st;
     __device__ bool skip() const { return is_done(st); }
-    __device__ void row(int i, double* acc) const {
-        const double ri = r[i];
-        const double zi = invd ? mul(ri, invd[i]) : ri;
-        z[i] = zi;
-        p[i] = zi;
-        acc[0] += ri * zi;
-    }
-    __device__ RedSlot slot() const { return rs; }
-    __device__ void fin(double* tot) const { FinStore<1>{red}(tot); }
-};
-
-struct BodyDCopy {
-    static constexpr int NR = 0;
-    const double* z;
-    double* p;
-    const PcgState* st;
-    __device__ bool skip() const { return is_done(st); }
-    __device__ void row(int i, double*) const { p[i] = z[i]; }
+    __device__ void row(int i, double*) const { z[i] = invd ? mul(r[i], invd[i]) : r[i]; }
     __device__ RedSlot slot() const { return {}; }
     __device__ void fin(double*) const {}
 };
 
-struct EpiDAp {  // Ap = A p ; partial p.Ap
-    static constexpr int NR = 1;
-    const double* p;
-    double* Ap;
+// w = A z with the iteration's four partial sums r.r, r.z, z.w, z.Ap_old — everything the
+// single-reduction recurrence needs, so one allreduce per iteration
+struct EpiDFused {
+    static constexpr int NR = 4;
+    const double* r;
+    const double* z;
+    const double* Ap;
+    double* w;
     RedSlot rs;
     double* red;
     const PcgState* st;
     __device__ bool skip() const { return is_done(st); }
-    __device__ void touch(int i) const { pf(p + i); }
+    __device__ void touch(int i) const {
+        pf(r + i);
+        pf(Ap + i);
+    }
     __device__ void row(int i, double s, double* acc) const {
-        Ap[i] = s;
-        acc[0] += p[i] * s;
+        w[i] = s;
+        const double ri = r[i], zi = z[i];
+        acc[0] += ri * ri;
+        acc[1] += ri * zi;
+        acc[2] += zi * s;
+        acc[3] += zi * Ap[i];
     }
     __device__ RedSlot slot() const { return rs; }
-    __device__ void fin(double* tot) const { FinStore<1>{red}(tot); }
+    __device__ void fin(double* tot) const { FinStore<4>{red}(tot); }
 };
 
-struct BodyDUpdate {  // x += alpha p ; r -= alpha Ap ; partial r.r (+ r.z)
-    static constexpr int NR = 2;
+// p = z + beta p, Ap = w + beta Ap (A p without a second SpMV), x += alpha p, r -= alpha Ap
+struct BodyDUpd {
+    static constexpr int NR = 0;
     double* x;
     double* r;
-    const double* p;
-    const double* Ap;
-    const double* invd;
-    double* z;
-    int kind;
-    RedSlot rs;
-    double* red;
-    const PcgState* st;
-    __device__ bool skip() const { return is_done(st); }
-    __device__ void row(int i, double* acc) const {
-        const double a = st->alpha;
-        x[i] = addd(x[i], mul(a, p[i]));
-        const double ri = addd(r[i], mul(-a, Ap[i]));
-        r[i] = ri;
-        acc[0] += ri * ri;
-        if (kind != IBMGPU_PC_SA) {
-            const double zi = kind == IBMGPU_PC_DIAGONAL ? mul(ri, invd[i]) : ri;
-            z[i] = zi;
-            acc[1] += ri * zi;
-        }
-    }
-    __device__ RedSlot slot() const { return rs; }
-    __device__ void fin(double* tot) const { FinStore<2>{red}(tot); }
-};
-
-struct BodyDP {
-    static constexpr int NR = 0;
-    const double* z;
     double* p;
+    double* Ap;
+    const double* z;
+    const double* w;
     const PcgState* st;
     __device__ bool skip() const { return is_done(st); }
-    __device__ void row(int i, double*) const { p[i] = addd(z[i], mul(st->beta, p[i])); }
+    __device__ void row(int i, double*) const {
+        const double b = st->beta, a = st->alpha;
+        const double pi = b == 0.0 ? z[i] : addd(z[i], mul(b, p[i]));  // first direction: p = z
+        const double api = b == 0.0 ? w[i] : addd(w[i], mul(b, Ap[i]));
+        p[i] = pi;
+        Ap[i] = api;
+        x[i] = addd(x[i], mul(a, pi));
+        r[i] = addd(r[i], mul(-a, api));
+    }
     __device__ RedSlot slot() const { return {}; }
     __device__ void fin(double*) const {}
 };
 
-// scalar recurrence of krylov.hpp:91-135 from the globally reduced sums
-enum { PH_INIT = 0, PH_RZ0 = 1, PH_ALPHA = 2, PH_REL = 3, PH_BETA = 4 };
+// Scalar recurrence from the globally reduced sums. PH_INIT: krylov.hpp:85-100 on r0.
+// PH_FUSED (sums r.r, r.z, z.w, z.Ap_old of iteration `it` = updates done so far):
+//   convergence of r_it exactly where krylov.hpp:126-127 tests it (it > 0), then
+//   beta = rz/rz_old, pAp = z.w + 2 beta z.Ap_old + beta^2 pAp_old  (= p.Ap for symmetric A),
+//   breakdown if pAp <= 0 (krylov.hpp:109-114), alpha = rz/pAp.
+// The iterates are krylov.hpp's up to rounding; `iterations` counts updates as the reference does.
+enum { PH_INIT = 0, PH_FUSED = 1 };
 
-__device__ void d_finish_iteration(PcgState& S) {
-    if (S.it >= S.max_iters) {
-        S.status = 1;
-        S.iterations = S.max_iters;
-        S.done = 1;
-        return;
-    }
-    ++S.it;
-}
-
-__global__ void k_dscal(PcgState* Sp, const double* red, int phase, int kind) {
+__global__ void k_dscal(PcgState* Sp, const double* red, int phase) {
     pdl_wait();
     PcgState& S = *Sp;
     if (phase == PH_INIT) {
-        S.it = 1;
+        S.it = 0;
         S.bnorm = __dsqrt_rn(red[0]);
         if (S.bnorm == 0.0) {
             S.status = 0, S.iterations = 0, S.rel = 0.0, S.done = 1, S.zero_x = 1;
@@ -297,33 +269,31 @@ __global__ void k_dscal(PcgState* Sp, const double* red, int phase, int kind) {
         return;
     }
     if (S.done) return;
-    if (phase == PH_RZ0) {
-        S.rz = red[0];
-    } else if (phase == PH_ALPHA) {
-        S.pAp = red[0];
-        if (!(S.pAp > 0.0)) {
-            S.status = 2, S.iterations = S.it - 1, S.done = 1;
-            return;
-        }
-        S.alpha = __ddiv_rn(S.rz, S.pAp);
-    } else if (phase == PH_REL) {
-        S.rel = __ddiv_rn(__dsqrt_rn(red[0]), S.bnorm);
+    const double rr = red[0], rz = red[1], zw = red[2], zap = red[3];
+    if (S.it > 0) {
+        S.rel = __ddiv_rn(__dsqrt_rn(rr), S.bnorm);
         if (S.hist) S.hist[S.it] = S.rel;
         S.hist_len = S.it + 1;
         if (S.rel <= S.rel_tol) {
             S.status = 0, S.iterations = S.it, S.done = 1;
             return;
         }
-        if (kind != IBMGPU_PC_SA) {
-            S.beta = __ddiv_rn(red[1], S.rz);
-            S.rz = red[1];
-            d_finish_iteration(S);
+        if (S.it >= S.max_iters) {
+            S.status = 1, S.iterations = S.max_iters, S.done = 1;
+            return;
         }
-    } else {  // PH_BETA
-        S.beta = __ddiv_rn(red[0], S.rz);
-        S.rz = red[0];
-        d_finish_iteration(S);
     }
+    const double beta = S.it == 0 ? 0.0 : __ddiv_rn(rz, S.rz);
+    const double pAp = S.it == 0 ? zw : addd(addd(zw, mul(mul(2.0, beta), zap)), mul(mul(beta, beta), S.pAp));
+    if (!(pAp > 0.0)) {
+        S.status = 2, S.iterations = S.it, S.done = 1;
+        return;
+    }
+    S.beta = beta;
+    S.alpha = __ddiv_rn(rz, pAp);
+    S.rz = rz;
+    S.pAp = pAp;
+    ++S.it;
 }
 
 // ---------------------------------------------------------------- distributed pieces
@@ -396,7 +366,7 @@ struct RankData {
     DBuf<int> own0_dev;
     DMat A;  // the PCG matrix
     std::vector<std::unique_ptr<DLev>> lev;
-    DBuf<double> b, x, r, z, p, Ap, invd;  // x, r, p extended (A0 halo)
+    DBuf<double> b, x, r, z, p, Ap, w, invd;  // x, r, z extended (A0 halo)
     DBuf<double> bD, xD;                    // full level-D vectors (replicated part)
     DBuf<PcgState> st;
     DBuf<double> red, partials;
@@ -540,7 +510,7 @@ void spmv_red(Ctx* c, const Mat* M, double* red, XF xf, Epi epi, cudaStream_t s)
 // level l's restriction feeds the replicated part
 inline bool rk_switch(const Dist* d, int l) { return l == d->D - 1; }
 
-// One distributed V(1,1) cycle z = M^{-1} r on every local rank; r.z partial -> red[0].
+// One distributed V(1,1) cycle z = M^{-1} r on every local rank.
 void dist_vcycle(Dist* d) {
     Ctx* c = d->c;
     cudaStream_t s = c->stream;
@@ -585,11 +555,8 @@ void dist_vcycle(Dist* d) {
             const int* done = &rk->st.p->done;
             if (l > 0) {
                 launch_spmv(c, L.A.m, XPlain{L.x.p}, EpiPostSmooth{L.wd.p, L.b.p, L.x.p, L.xo.p, done}, s);
-            } else {
-                spmv_red(c, L.A.m, rk->red.p, XPlain{L.x.p},
-                         EpiPostSmoothDot<FinStore<1>>{L.wd.p, rk->r.p, L.x.p, rk->z.p, done,
-                                                       RedSlot{rk->partials.p, nullptr}, FinStore<1>{rk->red.p}},
-                         s);
+            } else {  // z (r.z is reduced with the next SpMV's sums)
+                launch_spmv(c, L.A.m, XPlain{L.x.p}, EpiPostSmooth{L.wd.p, rk->r.p, L.x.p, rk->z.p, done}, s);
             }
         }
     }
@@ -603,37 +570,33 @@ namespace ibmgpu {
 namespace {
 
 void scal_all(Dist* d, int phase) {
-    for (auto& rk : d->ranks)
-        launch_k(d->c, k_dscal, 1, 1, d->c->stream, rk->st.p, (const double*)rk->red.p, phase, d->kind);
+    for (auto& rk : d->ranks) launch_k(d->c, k_dscal, 1, 1, d->c->stream, rk->st.p, (const double*)rk->red.p, phase);
 }
 
-// krylov.hpp:104-131, every local rank; scalars stay on the device
+// One iteration of the single-reduction PCG on every local rank; scalars stay on the device.
 void enqueue_iteration(Dist* d) {
     Ctx* c = d->c;
     cudaStream_t s = c->stream;
-    const int kind = d->kind;
     auto red = [](RankData& rk) { return rk.red.p; };
     auto rslot = [](RankData& rk) { return RedSlot{rk.partials.p, nullptr}; };
-    exchange(d, [](RankData& rk) -> DMat& { return rk.A; }, [](RankData& rk) { return rk.p.p; });
-    for (auto& rk : d->ranks)
-        spmv_red(c, rk->A.m, rk->red.p, XPlain{rk->p.p}, EpiDAp{rk->p.p, rk->Ap.p, rslot(*rk), rk->red.p, rk->st.p},
-                 s);
-    allreduce(d, red, 1);
-    scal_all(d, PH_ALPHA);
-    for (auto& rk : d->ranks)
-        launch_elem(c, rk->n_own, elem_grid(c, rk->n_own),
-                    BodyDUpdate{rk->x.p, rk->r.p, rk->p.p, rk->Ap.p, rk->invd.p, rk->z.p, kind, rslot(*rk), rk->red.p,
-                                rk->st.p},
-                    s);
-    allreduce(d, red, 2);
-    scal_all(d, PH_REL);
-    if (kind == IBMGPU_PC_SA) {
+    if (d->kind == IBMGPU_PC_SA) {
         dist_vcycle(d);
-        allreduce(d, red, 1);
-        scal_all(d, PH_BETA);
+    } else {
+        for (auto& rk : d->ranks)
+            if (rk->n_own)
+                launch_elem(c, rk->n_own, elem_grid(c, rk->n_own), BodyDPrecond{rk->r.p, rk->invd.p, rk->z.p, rk->st.p},
+                            s);
     }
+    exchange(d, [](RankData& rk) -> DMat& { return rk.A; }, [](RankData& rk) { return rk.z.p; });
     for (auto& rk : d->ranks)
-        if (rk->n_own) launch_elem(c, rk->n_own, elem_grid(c, rk->n_own), BodyDP{rk->z.p, rk->p.p, rk->st.p}, s);
+        spmv_red(c, rk->A.m, rk->red.p, XPlain{rk->z.p},
+                 EpiDFused{rk->r.p, rk->z.p, rk->Ap.p, rk->w.p, rslot(*rk), rk->red.p, rk->st.p}, s);
+    allreduce(d, red, 4);  // the iteration's only scalar collective
+    scal_all(d, PH_FUSED);
+    for (auto& rk : d->ranks)
+        if (rk->n_own)
+            launch_elem(c, rk->n_own, elem_grid(c, rk->n_own),
+                        BodyDUpd{rk->x.p, rk->r.p, rk->p.p, rk->Ap.p, rk->z.p, rk->w.p, rk->st.p}, s);
 }
 
 void capture_iteration(Dist* d) {
@@ -750,10 +713,11 @@ Dist* dist_create(Ctx* c, Mat* A, int kind, Hier* h, const int* owner0, int virt
         rk->own0_dev.alloc(c, no);
         h2d(c, rk->own0_dev.p, PA.own.data(), PA.own.size());
         rk->b.alloc(c, no);
-        rk->z.alloc(c, no);
+        rk->z.alloc(c, no + (size_t)PA.n_halo());
         rk->Ap.alloc(c, no);
+        rk->w.alloc(c, no);
         rk->x.alloc(c, no + (size_t)PA.n_halo());
-        rk->p.alloc(c, no + (size_t)PA.n_halo());
+        rk->p.alloc(c, no);
         if (kind == IBMGPU_PC_DIAGONAL) {
             std::vector<double> iv;
             for (int g : PA.own) iv.push_back(invd_full[(size_t)g]);
@@ -801,7 +765,7 @@ Dist* dist_create(Ctx* c, Mat* A, int kind, Hier* h, const int* owner0, int virt
         }
         rk->st.alloc(c, 1);
         rk->red.alloc(c, 4);
-        rk->partials.alloc(c, (size_t)std::max(grid, 1) * 2);
+        rk->partials.alloc(c, (size_t)std::max(grid, 1) * 4);
         CK(cudaMallocHost(&rk->host_st, sizeof(PcgState)));
         d->ranks.push_back(std::move(rk));
     }
@@ -816,7 +780,6 @@ void dist_solve(Dist* d, const double* b_full, double* x_full, const ibm_solver_
     validate_params(prm);
     Ctx* c = d->c;
     cudaStream_t s = c->stream;
-    const int kind = d->kind;
     if (d->n == 0) {
         if (res) *res = ibm_solve_result{0, 0.0, 0, 0};
         return;
@@ -837,31 +800,20 @@ void dist_solve(Dist* d, const double* b_full, double* x_full, const ibm_solver_
         CK(cudaMemcpyAsync(rk->st.p, &H, sizeof(PcgState), cudaMemcpyHostToDevice, s));
     }
     auto red = [](RankData& rk) { return rk.red.p; };
-    auto scal = [&](int phase) {
-        for (auto& rk : d->ranks) launch_k(c, k_dscal, 1, 1, s, rk->st.p, (const double*)rk->red.p, phase, kind);
-    };
     auto rslot = [](RankData& rk) { return RedSlot{rk.partials.p, nullptr}; };
+    for (auto& rk : d->ranks)
+        if (rk->n_own) {  // the recurrence reads p and Ap of "iteration -1" with beta = 0
+            CK(cudaMemsetAsync(rk->p.p, 0, sizeof(double) * (size_t)rk->n_own, s));
+            CK(cudaMemsetAsync(rk->Ap.p, 0, sizeof(double) * (size_t)rk->n_own, s));
+        }
     // r = b - A x0
     exchange(d, [](RankData& rk) -> DMat& { return rk.A; }, [](RankData& rk) { return rk.x.p; });
     for (auto& rk : d->ranks)
         spmv_red(c, rk->A.m, rk->red.p, XPlain{rk->x.p}, EpiDInit{rk->b.p, rk->r.p, rslot(*rk), rk->red.p}, s);
     allreduce(d, red, 2);
-    scal(PH_INIT);
+    scal_all(d, PH_INIT);
     for (auto& rk : d->ranks)
         if (rk->n_own) launch_elem(c, rk->n_own, elem_grid(c, rk->n_own), BodyDZeroX{rk->x.p, rk->st.p}, s);
-    if (kind == IBMGPU_PC_SA) {
-        dist_vcycle(d);
-        allreduce(d, red, 1);
-        scal(PH_RZ0);
-        for (auto& rk : d->ranks)
-            if (rk->n_own) launch_elem(c, rk->n_own, elem_grid(c, rk->n_own), BodyDCopy{rk->z.p, rk->p.p, rk->st.p}, s);
-    } else {
-        for (auto& rk : d->ranks)
-            launch_elem(c, rk->n_own, elem_grid(c, rk->n_own),
-                        BodyDInitZ{rk->r.p, rk->invd.p, rk->z.p, rk->p.p, rslot(*rk), rk->red.p, rk->st.p}, s);
-        allreduce(d, red, 1);
-        scal(PH_RZ0);
-    }
     PcgState* H0 = d->ranks[0]->host_st;
     CK(cudaMemcpyAsync(H0, d->ranks[0]->st.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
     sync(c);

@@ -207,7 +207,8 @@ class _Rank:
         return x + e["wd"][:n] * (b_own - self.spmv(PA, self.halo(PA, x)))
 
     def pcg(self, b_full, tol=1e-5, max_iters=200):
-        """krylov.hpp:70-136 with dist.cu's reductions (rank partials + allreduce)."""
+        """krylov.hpp:70-136 in dist.cu's single-reduction form: w = A z and ONE allreduce of
+        {r.r, r.z, z.w, z.Ap_old} per iteration; A p = w + beta Ap_old, p.Ap by recurrence."""
         P = self.pA
         b = b_full[P.own]
         x = np.zeros(len(b))
@@ -216,23 +217,26 @@ class _Rank:
         bnorm = np.sqrt(bb)
         if np.sqrt(rr) / bnorm <= tol:
             return x, 0
-        z = self.vcycle(0, r)
-        rz = self.allreduce([r @ z])[0]
-        p = z.copy()
-        for it in range(1, max_iters + 1):
-            Ap = self.spmv(P, self.halo(P, p))
-            pAp = self.allreduce([p @ Ap])[0]
+        p, Ap = np.zeros(len(b)), np.zeros(len(b))
+        rz_old = pAp_old = 0.0
+        it = 0
+        while True:
+            z = self.vcycle(0, r)
+            w = self.spmv(P, self.halo(P, z))
+            rr, rz, zw, zap = self.allreduce([r @ r, r @ z, z @ w, z @ Ap])
+            if it > 0:
+                if np.sqrt(rr) / bnorm <= tol or it >= max_iters:
+                    return x, it
+            beta = 0.0 if it == 0 else rz / rz_old
+            pAp = zw if it == 0 else zw + 2.0 * beta * zap + beta * beta * pAp_old
+            assert pAp > 0
             alpha = rz / pAp
+            p = z + beta * p
+            Ap = w + beta * Ap
             x += alpha * p
             r -= alpha * Ap
-            rr = self.allreduce([r @ r])[0]
-            if np.sqrt(rr) / bnorm <= tol:
-                return x, it
-            z = self.vcycle(0, r)
-            rz_new = self.allreduce([r @ z])[0]
-            p = z + (rz_new / rz) * p
-            rz = rz_new
-        return x, max_iters
+            rz_old, pAp_old = rz, pAp
+            it += 1
 
 
 def _worker(rank, R, port, min_rows, q):
