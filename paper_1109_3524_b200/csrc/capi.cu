@@ -62,7 +62,8 @@ int ibmgpu_init(int device, int nranks, int rank, const void* nccl_id, ibmgpu_ct
         unsigned long long thr = ~0ull;  // keep freed blocks cached in the pool
         CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
         need(nranks == 1 || nccl_id != nullptr, "init: multi-rank context needs an NCCL unique id");
-        if (nranks > 1) nccl_comm_init(c, nccl_id);
+        // nranks == 1 with an id: a one-rank NCCL communicator (exercises the NCCL code path)
+        if (nranks > 1 || nccl_id) nccl_comm_init(c, nccl_id);
     });
     if (rc) {
         if (out) *out = nullptr;
@@ -338,7 +339,7 @@ int ibmgpu_dist_create(ibmgpu_ctx_t c, ibmgpu_mat_t A, int precond, ibmgpu_hier_
                        int virtual_ranks, int min_dist_rows, ibmgpu_dist_t* out) {
     return guard(c, [&] {
         need(A && owner && out, "dist_create: null argument");
-        need(c->nranks == 1 || virtual_ranks <= 1, "dist_create: virtual ranks need a single-rank context");
+        need(!c->nccl || virtual_ranks <= 1, "dist_create: virtual ranks need a context without NCCL");
         *out = dist_create(c, A, precond, hier, owner, virtual_ranks, min_dist_rows);
     });
 }

@@ -452,7 +452,7 @@ void exchange(Dist* d, GetM gm, GetV gv) {
 
 template <class GetV>
 void allreduce(Dist* d, GetV gv, int n) {
-    if (d->R == 1 || n == 0) return;
+    if (n == 0 || (d->loop && d->R == 1)) return;
     Ctx* c = d->c;
     if (d->loop) {
         RankPtrs P{};
@@ -651,7 +651,7 @@ Dist* dist_create(Ctx* c, Mat* A, int kind, Hier* h, const int* owner0, int virt
     d->A = A;
     d->h = kind == IBMGPU_PC_SA ? h : nullptr;
     d->kind = kind;
-    d->loop = c->nranks == 1;
+    d->loop = c->nccl == nullptr;
     d->R = d->loop ? std::max(1, virtual_ranks) : c->nranks;
     require(!d->loop || d->R <= kMaxLoop, "dist: at most 16 loopback ranks");
     const int R = d->R;

@@ -510,9 +510,9 @@ struct ibmgpu_stepper {
         if (!dist_stale && dist) return;
         dist_destroy(dist);
         dist = nullptr;
-        const int R = c->nranks > 1 ? c->nranks : dist_ranks;
+        const int R = c->nccl ? c->nranks : dist_ranks;
         const auto own = lambda_owner(R);
-        dist = dist_create(c, lhs2, IBMGPU_PC_SA, hier, own.data(), c->nranks > 1 ? 1 : dist_ranks, dist_min_rows);
+        dist = dist_create(c, lhs2, IBMGPU_PC_SA, hier, own.data(), c->nccl ? 1 : dist_ranks, dist_min_rows);
         if (b2.n != (size_t)n_lambda) {
             b2.alloc(c, (size_t)n_lambda);
             x2.alloc(c, (size_t)n_lambda);
@@ -811,7 +811,7 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
         return;
     }
     // stage 2 (single GPU: one graph launch; distributed: row-slab PCG, dist.cu)
-    const bool distributed = S->dist_ranks > 0 || c->nranks > 1;
+    const bool distributed = S->dist_ranks > 0 || c->nccl != nullptr;
     if (distributed) S->ensure_dist();
     PcgPlan* P2 = distributed ? nullptr : pcg_plan(c, S->lhs2, IBMGPU_PC_SA, S->hier);
     double* b2 = distributed ? S->b2.p : P2->b.p;
@@ -1063,8 +1063,8 @@ int ibmgpu_stepper_bodies(ibmgpu_stepper_t S, double* x, double* y, double* ubx,
 int ibmgpu_stepper_distribute(ibmgpu_stepper_t S, int virtual_ranks, int min_dist_rows) {
     return sguard(S, [&] {
         require(virtual_ranks >= 0, "stepper_distribute: virtual_ranks must be >= 0");
-        require(S->c->nranks == 1 || virtual_ranks <= 1, "stepper_distribute: virtual ranks need a single-rank context");
-        S->dist_ranks = S->c->nranks > 1 ? S->c->nranks : virtual_ranks;
+        require(!S->c->nccl || virtual_ranks <= 1, "stepper_distribute: virtual ranks need a context without NCCL");
+        S->dist_ranks = S->c->nccl ? S->c->nranks : virtual_ranks;
         S->dist_min_rows = min_dist_rows;
         S->dist_stale = true;
         dist_destroy(S->dist);

@@ -134,3 +134,26 @@ def test_distributed_stepper_matches_single(name, steps):
         assert abs(fa["cd"] - fb["cd"]) <= 1e-6 * abs(fa["cd"])
     b.distribute(0)  # back to the single-GPU graph solve
     assert b.advance().ok
+
+
+def test_nccl_backend_one_rank(small):
+    """The NCCL code path on the one GPU available: a one-rank communicator, so every allreduce
+    and the final gather of x go through ncclAllReduce (captured in the per-iteration graph)."""
+    d, A, h, single = small
+    ctx = ibm.Context(0, nranks=1, rank=0, nccl_id=ibm.nccl_unique_id())
+    A1 = ibm.SparseMatrix.from_host(H.small_mat(d, "lhs2"), ctx=ctx)
+    n_b = int(d["dims"][4])
+    h1 = ibm.build_sa_hierarchy(A1, ibm.SaOptions(keep_fine_tail=2 * n_b))
+    ds = ibm.DistSolver(A1, ibm.SaPreconditioner(h1), np.zeros(A1.rows(), np.int32))
+    assert ds.info()["loopback"] == 0 and ds.info()["nranks"] == 1
+    r = ds.solve(d["bench_b"])
+    assert r.converged() and abs(r.iterations - single.iterations) <= 2
+    assert np.max(np.abs(r.x - d["bench_x"])) <= 1e-6 * np.max(np.abs(d["bench_x"]))
+    st = ibm.Stepper(H.case("cylinder_re40_smoke"), ctx=ctx)
+    ref = ibm.Stepper(H.case("cylinder_re40_smoke"))
+    st.distribute(virtual_ranks=1, min_dist_rows=0)
+    for _ in range(2):
+        ra, rb = ref.advance(), st.advance()
+        assert ra.ok and rb.ok and abs(ra.solve2_iters - rb.solve2_iters) <= 2
+    la, lb = ref.get("lambda"), st.get("lambda")
+    assert np.linalg.norm(la - lb) <= 1e-6 * np.linalg.norm(la)
