@@ -16,6 +16,8 @@
 #include <cub/cub.cuh>
 
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 
@@ -73,16 +75,21 @@ __global__ void __launch_bounds__(256) k_lfmis(int n, const int* __restrict__ sr
         int st = i < n ? UNDEC : NOTSEED;
         wstat[w][lane] = st;
         __syncwarp();
+        // resume cursor: every candidate before (cq, cr) was NOTSEED when last seen, and NOTSEED is
+        // final, so a re-scan starts at the first candidate that was still undecided
+        const int ob = i < n ? srp[i] : 0, oe = i < n ? srp[i + 1] : 0;
+        int cq = ob - 1, cr = -1;
+        bool fresh = true;
         while (__any_sync(kFull, st == UNDEC)) {
             if (st == UNDEC) {
                 bool pending = false, hit = false;
+                int nq = cq, nr = cr;
                 // u = i itself and u in out(i)
-                const int ob = srp[i], oe = srp[i + 1];
-                for (int q = ob - 1; q < oe && !hit; ++q) {
+                for (int q = cq; q < oe && !hit; ++q) {
                     const int u = q < ob ? i : sci[q];
                     // candidates s = u (if u < i) and s in in(u) with s < i
                     const int tb = trp[u], te = trp[u + 1];
-                    for (int r = tb - 1; r < te; ++r) {
+                    for (int r = (q == cq && !fresh) ? cr : tb - 1; r < te; ++r) {
                         const int s = r < tb ? u : tci[r];
                         if (s >= i) {
                             if (r >= tb) break;  // in-lists are sorted: the rest are >= i
@@ -93,13 +100,18 @@ __global__ void __launch_bounds__(256) k_lfmis(int n, const int* __restrict__ sr
                             hit = true;
                             break;
                         }
-                        if (ss == UNDEC) pending = true;
+                        if (ss == UNDEC && !pending) {
+                            pending = true;
+                            nq = q, nr = r;
+                        }
                     }
                 }
                 if (hit)
                     st = NOTSEED;
                 else if (!pending)
                     st = SEED;
+                else
+                    cq = nq, cr = nr, fresh = false;
                 if (st != UNDEC) {
                     gstat[i] = st;
                     wstat[w][lane] = st;
@@ -354,6 +366,28 @@ void build_fused_coarse(Ctx* c, Hier* h) {
 
 }  // namespace
 
+namespace {
+// IBMGPU_SETUP_PROFILE=1: per-phase wall times of the hierarchy build on stderr (syncs per phase)
+struct SetupClock {
+    Ctx* c;
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    explicit SetupClock(Ctx* c_) : c(c_) {
+        const char* e = std::getenv("IBMGPU_SETUP_PROFILE");
+        on = e && e[0] == '1';
+        t = std::chrono::steady_clock::now();
+    }
+    void lap(const char* what, int lev) {
+        if (!on) return;
+        sync(c);
+        const auto n = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[sa_build] L%d %-10s %8.3f ms\n", lev, what,
+                     std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+}  // namespace
+
 // Strength graph + exact greedy aggregation; returns aggregate count, agg sized n_core.
 int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& agg) {
     agg.alloc(c, (size_t)std::max(n_core, 1));
@@ -376,7 +410,9 @@ int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& 
     k_strength<<<blocks(n_core), 256, 0, c->stream>>>(n_core, theta, A->rp.p, A->ci.p, A->v.p, diag.p, nullptr,
                                                       S.rp.p, S.ci.p);
     CK_LAUNCH(c);
+    SetupClock clk(c);
     Mat* St = transpose(c, &S);  // in-neighbour lists (sorted by source row)
+    clk.lap("  agg:S+St", -2);
 
     // pass 1
     DBuf<int> status(c, (size_t)n_core), seedflag(c, (size_t)n_core), seed_id(c, (size_t)n_core + 1);
@@ -388,6 +424,7 @@ int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& 
     const int grid = std::max(1, std::min(per_sm * c->num_sms, (n_core + 255) / 256));
     k_lfmis<<<grid, 256, 0, c->stream>>>(n_core, S.rp.p, S.ci.p, St->rp.p, St->ci.p, status.p, ticket.p);
     CK_LAUNCH(c);
+    clk.lap("  agg:lfmis", -2);
     k_seed_flags<<<blocks(n_core), 256, 0, c->stream>>>(n_core, status.p, seedflag.p);
     CK_LAUNCH(c);
     exclusive_scan_total(c, seedflag.p, seed_id.p, n_core);
@@ -407,6 +444,7 @@ int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& 
         CK_LAUNCH(c);
         if (!d2h_scalar(c, changed.p)) break;
     }
+    clk.lap("  agg:cover+p2", -2);
     d2d(c, agg.p, agg1.p, (size_t)n_core);
     k_pass2_apply<<<blocks(n_core), 256, 0, c->stream>>>(n_core, agg1.p, tgt.p, agg.p);
     CK_LAUNCH(c);
@@ -425,8 +463,10 @@ int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& 
     return n_seeds + n3;
 }
 
+
 Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
     require(A_fine->rows == A_fine->cols, "sa: square matrix required");
+    SetupClock clk(c);
     static std::atomic<long long> next_id{1};
     auto* h = new Hier();
     h->id = next_id++;
@@ -439,6 +479,7 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
             const int n_core = A->rows - tail;
             auto L = std::make_unique<Level>();
             const int n_agg = aggregate_device(c, A, theta_l, n_core, L->agg);
+            clk.lap("aggregate", lev);
             if (n_agg >= n_core) {
                 h->stalled = true;
                 break;
@@ -457,6 +498,7 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
             }
             const double rho = rho_dinv_a(c, A, L->invd.p, o.power_iterations);
             const double omega = (4.0 / 3.0) / rho;
+            clk.lap("rho", lev);
             L->wd.alloc(c, (size_t)n);
             k_invd<<<blocks(n), 256, 0, c->stream>>>(n, d.p, omega, L->invd.p, L->wd.p, zero.p);
             CK_LAUNCH(c);
@@ -479,8 +521,11 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
             delete Ptent;
             Mat* P = tail > 0 ? identity_tail_append(c, Pcore, n_core, n_agg, tail) : Pcore;
             if (tail > 0) delete Pcore;
+            clk.lap("P", lev);
             Mat* Pt = transpose(c, P);
+            clk.lap("transpose", lev);
             Mat* Ac = triple_product(c, Pt, A, P, std::max(1, Pt->rows), nullptr, nullptr);
+            clk.lap("galerkin", lev);
 
             L->A = A;
             L->P = P;
@@ -504,6 +549,7 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
             lv.r.alloc(c, n);
             lv.xo.alloc(c, n);
         }
+        clk.lap("plans", -1);
         h->coarse_inv.alloc(c, (size_t)h->n_c * h->n_c);
         dense_spd_inverse(c, h->coarse_A, h->coarse_inv.p);
         h->coarse_tiles.alloc(c, packed_tiles_doubles(h->n_c));
@@ -513,6 +559,7 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
         h->cb.alloc(c, (size_t)h->n_c);
         h->cx.alloc(c, (size_t)h->n_c);
         build_fused_coarse(c, h);
+        clk.lap("coarse", -1);
         sync(c);
     } catch (...) {
         delete h;

@@ -1,5 +1,7 @@
 // capi.cu — extern "C" entry points of include/ibmgpu.h (context, memory, CSR, solvers).
 // Every call is wrapped so that C++ exceptions become IBMGPU_E* codes + ibmgpu_last_error().
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "amg.cuh"
@@ -61,6 +63,25 @@ int ibmgpu_init(int device, int nranks, int rank, const void* nccl_id, ibmgpu_ct
         CK(cudaDeviceGetDefaultMemPool(&pool, device));
         unsigned long long thr = ~0ull;  // keep freed blocks cached in the pool
         CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        // Pre-map part of the pool once per device: the SpGEMM sort buffers of a hierarchy rebuild
+        // (up to ~2 GB at 600k rows) otherwise map fresh pages mid-setup, which made identical
+        // rebuilds vary 65-500 ms (IBMGPU_POOL_RESERVE_MB, default 8192; 0 disables).
+        static bool reserved[64] = {};
+        const char* rv = std::getenv("IBMGPU_POOL_RESERVE_MB");
+        const size_t mb = rv ? std::strtoull(rv, nullptr, 10) : 8192;
+        if (mb && device >= 0 && device < 64 && !reserved[device]) {
+            size_t free_b = 0, total_b = 0;
+            CK(cudaMemGetInfo(&free_b, &total_b));
+            const size_t want = std::min(mb << 20, free_b / 4);
+            void* p = nullptr;
+            if (cudaMallocAsync(&p, want, c->stream) == cudaSuccess) {
+                CK(cudaFreeAsync(p, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+            } else {
+                cudaGetLastError();
+            }
+            reserved[device] = true;
+        }
         need(nranks == 1 || nccl_id != nullptr, "init: multi-rank context needs an NCCL unique id");
         // nranks == 1 with an id: a one-rank NCCL communicator (exercises the NCCL code path)
         if (nranks > 1 || nccl_id) nccl_comm_init(c, nccl_id);

@@ -14,6 +14,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.cuh"
@@ -372,7 +375,16 @@ Mat* esc_chunk(Ctx* c, const Mat* A, const int* arow_of, int r0, int r1, const M
     k_expand<<<blocks(na), 256, 0, c->stream>>>(r0, k0, k1, arow_of, A->ci.p, A->v.p, B->rp.p, B->ci.p, B->v.p,
                                                  pos.p, 0, kin.p, vin.p);
     CK_LAUNCH(c);
-    sort_pairs(c, kin.p, kout.p, vin.p, vout.p, n, 32 + bits_for(rows + 1));
+    if (std::getenv("IBMGPU_SETUP_PROFILE")) {
+        sync(c);
+        const auto t0 = std::chrono::steady_clock::now();
+        sort_pairs(c, kin.p, kout.p, vin.p, vout.p, n, 32 + bits_for(rows + 1));
+        sync(c);
+        std::fprintf(stderr, "[esc] rows %d products %lld sort %.3f ms\n", rows, n,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    } else {
+        sort_pairs(c, kin.p, kout.p, vin.p, vout.p, n, 32 + bits_for(rows + 1));
+    }
     kin.release();
     vin.release();
     DBuf<long long> start;
