@@ -201,11 +201,11 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
                                                          const int* __restrict__ off, const int* __restrict__ ci,
                                                          const double* __restrict__ v, XF xf, Epi epi) {
     constexpr int NR = Epi::NR;
-    pdl_wait();
-    if (epi.skip()) return;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
+    // The matrix is constant for the whole solve, so its first slice entries are loaded BEFORE
+    // griddepcontrol.wait: under PDL they stream in while the predecessor kernel drains.
     const int n_slices = (rows + 31) >> 5;
     int ix[kSellRows], base[kSellRows], width[kSellRows], len[kSellRows];
 #pragma unroll
@@ -219,9 +219,6 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
         base[q] = beg + (i & 31);
         len[q] = i < rows ? __ldg(rp + i + 1) - __ldg(rp + i) : 0;
         ix[q] = i;
-        if constexpr (requires { epi.touch(0); }) {
-            if (i < rows) epi.touch(i);
-        }
     }
     int c[kSellRows][kSellU];
     double a[kSellRows][kSellU];
@@ -233,6 +230,13 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
                 c[q][u] = __ldg(ci + base[q] + 32 * u);
                 a[q][u] = __ldg(v + base[q] + 32 * u);
             }
+    pdl_wait();
+    if (epi.skip()) return;
+    if constexpr (requires { epi.touch(0); }) {
+#pragma unroll
+        for (int q = 0; q < kSellRows; ++q)
+            if (ix[q] < rows) epi.touch(ix[q]);
+    }
     double s[kSellRows];
 #pragma unroll
     for (int q = 0; q < kSellRows; ++q) {
@@ -269,26 +273,27 @@ struct StencilPlan {
 template <class XF, class Epi>
 __global__ void __launch_bounds__(kBlock, 8) k_spmv_stencil(int rows, StencilPlan P, XF xf, Epi epi) {
     constexpr int NR = Epi::NR;
-    pdl_wait();
-    if (epi.skip()) return;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
     const int i = blockIdx.x * kBlock + threadIdx.x;
     const bool live = i < rows;
+    // mask and band values are constant for the solve: loaded before griddepcontrol.wait
     const unsigned m = live ? __ldg(P.mask + i) : 0u;
-    if constexpr (requires { epi.touch(0); }) {
-        if (live) epi.touch(i);
-    }
     const int S = (m & 64u) ? P.S2 : P.S1;
     double a[5], xv[5];
     const int col[5] = {i - S, i - 1, i, i + 1, i + S};
 #pragma unroll
     for (int q = 0; q < 5; ++q)
-        if (m & (1u << q)) {
-            a[q] = __ldg(P.v + (size_t)q * rows + i);
-            xv[q] = xf(col[q]);
-        }
+        if (m & (1u << q)) a[q] = __ldg(P.v + (size_t)q * rows + i);
+    pdl_wait();
+    if (epi.skip()) return;
+    if constexpr (requires { epi.touch(0); }) {
+        if (live) epi.touch(i);
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q)
+        if (m & (1u << q)) xv[q] = xf(col[q]);
     double s = 0.0;
 #pragma unroll
     for (int q = 0; q < 5; ++q)
@@ -346,12 +351,12 @@ __global__ void __launch_bounds__(kBlock, 4) k_spmv_sellw(int rows, const int* _
                                                           const double* __restrict__ csr_v) {
     constexpr int NR = Epi::NR;
     constexpr int U = 4;
-    pdl_wait();
-    if (epi.skip()) return;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
     if (blockIdx.x >= sblocks) {
+        pdl_wait();
+        if (epi.skip()) return;
         const int w = (blockIdx.x - sblocks) * (kBlock / 32) + (threadIdx.x >> 5);
         const int lane = threadIdx.x & 31;
         if (w < n_long) {
@@ -371,9 +376,6 @@ __global__ void __launch_bounds__(kBlock, 4) k_spmv_sellw(int rows, const int* _
     const int base = beg + (i & 31);
     const int row = i < rows ? __ldg(perm + i) : -1;
     const int len = row >= 0 ? __ldg(rp + row + 1) - __ldg(rp + row) : 0;
-    if constexpr (requires { epi.touch(0); }) {
-        if (row >= 0) epi.touch(row);
-    }
     int c0[U];
     double a0[U];
 #pragma unroll
@@ -382,6 +384,11 @@ __global__ void __launch_bounds__(kBlock, 4) k_spmv_sellw(int rows, const int* _
             c0[u] = __ldg(ci + base + 32 * u);
             a0[u] = __ldg(v + base + 32 * u);
         }
+    pdl_wait();  // everything above is the (constant) matrix
+    if (epi.skip()) return;
+    if constexpr (requires { epi.touch(0); }) {
+        if (row >= 0) epi.touch(row);
+    }
     double s = 0.0;
     for (int k0 = 0; k0 < width; k0 += U) {
         int c1[U];
@@ -429,12 +436,12 @@ __global__ void __launch_bounds__(kBlock) k_spmv_adapt(AdaptPlan pl, const int* 
                                                        const int* __restrict__ ci, const double* __restrict__ v,
                                                        XF xf, Epi epi) {
     constexpr int NR = Epi::NR;
+    const int4 m = __ldg(pl.meta + blockIdx.x);  // plan and matrix are constant: read before the wait
     pdl_wait();
     if (epi.skip()) return;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
-    const int4 m = __ldg(pl.meta + blockIdx.x);
     const int tpr = m.z;
     if (tpr == 0) {  // one chunk of a long row, whole CTA
         const int row = m.x, chunk = m.y;
