@@ -437,13 +437,13 @@ __global__ void __launch_bounds__(kBlock) k_spmv_adapt(AdaptPlan pl, const int* 
                                                        XF xf, Epi epi) {
     constexpr int NR = Epi::NR;
     const int4 m = __ldg(pl.meta + blockIdx.x);  // plan and matrix are constant: read before the wait
-    pdl_wait();
-    if (epi.skip()) return;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
     const int tpr = m.z;
     if (tpr == 0) {  // one chunk of a long row, whole CTA
+        pdl_wait();
+        if (epi.skip()) return;
         const int row = m.x, chunk = m.y;
         const int2 lr = __ldg(pl.lrow + m.w);
         const int kb = __ldg(rp + row) + chunk * kRowChunk;
@@ -482,25 +482,43 @@ __global__ void __launch_bounds__(kBlock) k_spmv_adapt(AdaptPlan pl, const int* 
     } else {
         const int r0 = m.x, r1 = m.y;
         const int lane = threadIdx.x & (tpr - 1), grp = threadIdx.x / tpr, ngrp = kBlock / tpr;
+        // the first pass's row bounds and first 4-wide batch are matrix data: issued before the wait
+        int c[4];
+        double a[4];
+        int i = r0 + grp, k = 0, e = 0;
+        auto load_batch = [&]() {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k + u * tpr < e) {
+                    c[u] = __ldg(ci + k + u * tpr);
+                    a[u] = __ldg(v + k + u * tpr);
+                }
+        };
+        if (i < r1) {
+            e = __ldg(rp + i + 1);
+            k = __ldg(rp + i) + lane;
+            load_batch();
+        }
+        pdl_wait();
+        if (epi.skip()) return;
         for (int base = r0; base < r1; base += ngrp) {
-            const int i = base + grp;
+            i = base + grp;
             double s = 0.0;
             if (i < r1) {
-                const int e = __ldg(rp + i + 1);
+                if (base != r0) {
+                    e = __ldg(rp + i + 1);
+                    k = __ldg(rp + i) + lane;
+                    load_batch();
+                }
                 // predicated 4-wide batches: a lane's last (partial) batch issues all its loads at
                 // once instead of one dependent index->gather chain per remaining entry
-                for (int k = __ldg(rp + i) + lane; k < e; k += 4 * tpr) {
-                    int c[4];
-                    double a[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (k + u * tpr < e) {
-                            c[u] = __ldg(ci + k + u * tpr);
-                            a[u] = __ldg(v + k + u * tpr);
-                        }
+                for (;;) {
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
                         if (k + u * tpr < e) s = addd(s, mul(a[u], xf(c[u])));
+                    k += 4 * tpr;
+                    if (k >= e) break;
+                    load_batch();
                 }
             }
             for (int o = tpr >> 1; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o, tpr);
