@@ -215,6 +215,8 @@ __global__ void __launch_bounds__(256) k_gemv(int n, const double* __restrict__ 
 
 // ---- packed symmetric inverse: lower-triangle 64x64 tiles, tile (I,J), J <= I, at I(I+1)/2+J
 constexpr int TS = 64;
+constexpr int TP = TS + 1;  // stored row pitch of a packed tile: the pad keeps row and column reads
+                            // of the smem copy bank-conflict free, and lets one bulk copy land it
 
 __global__ void k_pack_tiles(int n, const double* __restrict__ full, double* __restrict__ tiles) {
     const int t = blockIdx.x;
@@ -222,41 +224,67 @@ __global__ void k_pack_tiles(int n, const double* __restrict__ full, double* __r
     while ((I + 1) * (I + 2) / 2 <= t) ++I;
     while (I * (I + 1) / 2 > t) --I;
     const int J = t - I * (I + 1) / 2;
-    double* dst = tiles + (size_t)t * TS * TS;
-    for (int e = threadIdx.x; e < TS * TS; e += blockDim.x) {
-        const int r = I * TS + e / TS, cc = J * TS + e % TS;
-        dst[e] = (r < n && cc < n) ? full[(size_t)r * n + cc] : 0.0;
+    double* dst = tiles + (size_t)t * TS * TP;
+    for (int e = threadIdx.x; e < TS * TP; e += blockDim.x) {
+        const int rr = e / TP, cl = e % TP;
+        const int r = I * TS + rr, cc = J * TS + cl;
+        dst[e] = (cl < TS && r < n && cc < n) ? full[(size_t)r * n + cc] : 0.0;
     }
 }
 
 // one CTA per tile: row sums A_IJ x_J and (off-diagonal tiles) column sums A_IJ^T x_I, each in a
-// fixed order, from one read of the tile
-__global__ void __launch_bounds__(256) k_symv_tiles(int n, int nt, const double* __restrict__ tiles,
+// fixed order, from one read of the tile. The tile (33 KB, constant) arrives by one TMA bulk copy
+// (cp.async.bulk + mbarrier transaction count) issued before griddepcontrol.wait, so under PDL it
+// streams in while the predecessor drains and no thread spends registers staging it.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+__global__ void __launch_bounds__(128) k_symv_tiles(int n, int nt, const double* __restrict__ tiles,
                                                     const double* __restrict__ x, double* __restrict__ prow,
                                                     double* __restrict__ pcol, const int* done) {
-    pdl_wait();
-    if (done && *(volatile const int*)done) return;
-    __shared__ double A[TS][TS + 1];
+    __shared__ alignas(128) double A[TS][TP];
     __shared__ double xi[TS], xj[TS];
+    __shared__ alignas(8) unsigned long long bar;
+    constexpr unsigned kBytes = TS * TP * sizeof(double);
     const int t = blockIdx.x;
     int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
     while ((I + 1) * (I + 2) / 2 <= t) ++I;
     while (I * (I + 1) / 2 > t) --I;
     const int J = t - I * (I + 1) / 2;
-    const double* src = tiles + (size_t)t * TS * TS;
-    for (int e = threadIdx.x; e < TS * TS; e += blockDim.x) A[e / TS][e % TS] = __ldg(src + e);
-    if (threadIdx.x < TS) {
+    const unsigned bar_a = smem_u32(&bar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double* src = tiles + (size_t)t * TS * TP;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a), "r"(kBytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(&A[0][0])),
+                     "l"(src), "r"(kBytes), "r"(bar_a)
+                     : "memory");
+    }
+    pdl_wait();
+    const bool skip = done && *(volatile const int*)done;
+    if (!skip && threadIdx.x < TS) {
         const int gi = I * TS + threadIdx.x, gj = J * TS + threadIdx.x;
         xi[threadIdx.x] = gi < n ? x[gi] : 0.0;
         xj[threadIdx.x] = gj < n ? x[gj] : 0.0;
     }
+    unsigned landed = 0;  // the copy must land before the CTA may exit, even when skipping
+    while (!landed)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(landed)
+                     : "r"(bar_a), "r"(0u)
+                     : "memory");
     __syncthreads();
+    if (skip) return;
     if (threadIdx.x < TS) {
         const int r = threadIdx.x;
         double s = 0.0;
         for (int k = 0; k < TS; ++k) s += A[r][k] * xj[k];
         prow[(size_t)t * TS + r] = s;
-    } else if (threadIdx.x < 2 * TS && I != J) {
+    } else if (I != J) {
         const int cc = threadIdx.x - TS;
         double s = 0.0;
         for (int k = 0; k < TS; ++k) s += A[k][cc] * xi[k];
@@ -292,7 +320,7 @@ void pack_symmetric_tiles(Ctx* c, int n, const double* full, double* tiles) {
 
 size_t packed_tiles_doubles(int n) {
     const size_t nt = (size_t)(n + TS - 1) / TS;
-    return nt * (nt + 1) / 2 * TS * TS;
+    return nt * (nt + 1) / 2 * TS * TP;
 }
 size_t packed_partials_doubles(int n) {
     const size_t nt = (size_t)(n + TS - 1) / TS;
@@ -304,7 +332,7 @@ void launch_symv_packed(Ctx* c, int n, const double* tiles, const double* x, dou
     const int nt = (n + TS - 1) / TS;
     const int ntiles = nt * (nt + 1) / 2;
     if (ntiles == 0) return;
-    launch_k(c, k_symv_tiles, ntiles, 256, s, n, nt, tiles, x, prow, pcol, done);
+    launch_k(c, k_symv_tiles, ntiles, 128, s, n, nt, tiles, x, prow, pcol, done);
     launch_k(c, k_symv_combine, nt, TS, s, n, nt, (const double*)prow, (const double*)pcol, y, done);
 }
 
