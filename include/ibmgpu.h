@@ -214,6 +214,9 @@ int ibmgpu_stepper_hier(ibmgpu_stepper_t st, ibmgpu_hier_t* out);
 int ibmgpu_stepper_grid(ibmgpu_stepper_t st, int which, double* out, int* n);
 /* body points at the current time: x, y, ub_x, ub_y, ds (each n_b) */
 int ibmgpu_stepper_bodies(ibmgpu_stepper_t st, double* x, double* y, double* ubx, double* uby, double* ds);
+/* compute_vorticity (diagnostics.hpp:42-56) on the device: (nx-1)(ny-1) values at the interior
+ * vertices, row-major in j; *n receives the length (out may be NULL to query) */
+int ibmgpu_stepper_vorticity(ibmgpu_stepper_t st, double* out, int* n);
 /* time the last advance() spent in each device phase, from CUDA events (ms) */
 int ibmgpu_stepper_phase_ms(ibmgpu_stepper_t st, float* ms6);
 

@@ -117,6 +117,7 @@ _SIGS = [
     ("ibmgpu_stepper_grid", C.c_int, [_vp, C.c_int, _dp, _ip]),
     ("ibmgpu_stepper_bodies", C.c_int, [_vp, _dp, _dp, _dp, _dp, _dp]),
     ("ibmgpu_stepper_phase_ms", C.c_int, [_vp, C.POINTER(C.c_float)]),
+    ("ibmgpu_stepper_vorticity", C.c_int, [_vp, _dp, _ip]),
     ("ibmgpu_hostcase_open", C.c_int, [C.c_char_p, C.POINTER(CaseOverridesC), C.POINTER(_vp), _ip, C.c_char_p, C.c_int]),
     ("ibmgpu_hostcase_array", C.c_int, [_vp, C.c_char_p, _dp, _ip]),
     ("ibmgpu_hostcase_csr", C.c_int, [_vp, C.c_char_p, _ip, _ip, _ip, _ip, _ip, _dp]),

@@ -375,6 +375,27 @@ double host_from_bits(unsigned long long b) {
 
 }  // namespace
 
+namespace {
+// compute_vorticity (diagnostics.hpp:42-56): omega = dv/dx - du/dy at the interior vertices,
+// row-major in j, same operation order (bit-exact)
+__global__ void k_vorticity(int nx, int ny, const double* __restrict__ dx, const double* __restrict__ dy,
+                            const double* __restrict__ del_x, const double* __restrict__ del_y,
+                            const double* __restrict__ q, double* __restrict__ w) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long m = (long long)(nx - 1) * (ny - 1);
+    if (t >= m) return;
+    const int i = 1 + (int)(t % (nx - 1)), j = 1 + (int)(t / (nx - 1));
+    const long long n_u = (long long)(nx - 1) * ny;
+    auto u_id = [&](int i_f, int jj) { return (long long)(i_f - 1) + (long long)jj * (nx - 1); };
+    auto v_id = [&](int ii, int j_f) { return n_u + ii + (long long)(j_f - 1) * nx; };
+    const double dvdx = __ddiv_rn(__dsub_rn(__ddiv_rn(q[v_id(i, j)], dx[i]), __ddiv_rn(q[v_id(i - 1, j)], dx[i - 1])),
+                                  del_x[i - 1]);
+    const double dudy = __ddiv_rn(__dsub_rn(__ddiv_rn(q[u_id(i, j)], dy[j]), __ddiv_rn(q[u_id(i, j - 1)], dy[j - 1])),
+                                  del_y[j - 1]);
+    w[t] = __dsub_rn(dvdx, dudy);
+}
+}  // namespace
+
 struct ibmgpu_stepper {
     Ctx* c = nullptr;
     ibmhost::Case cfg;
@@ -1058,6 +1079,23 @@ int ibmgpu_stepper_bodies(ibmgpu_stepper_t S, double* x, double* y, double* ubx,
             ds[k] = b.ds;
         }
     return 0;
+}
+
+int ibmgpu_stepper_vorticity(ibmgpu_stepper_t S, double* out, int* n) {
+    return sguard(S, [&] {
+        Ctx* c = S->c;
+        const int nx = S->g.nx, ny = S->g.ny;
+        const long long m = (long long)(nx - 1) * (ny - 1);
+        require(m < (1ll << 31), "stepper_vorticity: grid too large");
+        if (n) *n = (int)m;
+        if (!out || m == 0) return;
+        DBuf<double> w(c, (size_t)m);
+        k_vorticity<<<(unsigned)((m + 255) / 256), 256, 0, c->stream>>>(nx, ny, S->dx.p, S->dy.p, S->del_x.p,
+                                                                        S->del_y.p, S->q.p, w.p);
+        CK_LAUNCH(c);
+        d2h(c, out, w.p, (size_t)m);
+        sync(c);
+    });
 }
 
 int ibmgpu_stepper_distribute(ibmgpu_stepper_t S, int virtual_ranks, int min_dist_rows) {

@@ -571,6 +571,14 @@ class Stepper:
                                                                     ("x", "y", "ub_x", "ub_y", "ds")]))
         return {k: v[:self.n_b] for k, v in out.items()}
 
+    def vorticity(self) -> np.ndarray:
+        """compute_vorticity (diagnostics.hpp:42-56) of the current q, on the device."""
+        n = C.c_int()
+        self.ctx.check(self.ctx.lib.ibmgpu_stepper_vorticity(self.h, None, C.byref(n)))
+        w = np.zeros(max(n.value, 1))
+        self.ctx.check(self.ctx.lib.ibmgpu_stepper_vorticity(self.h, _d(w), C.byref(n)))
+        return w[:n.value]
+
     def distribute(self, virtual_ranks: int = 0, min_dist_rows: int = 200000):
         """Row-slab solve 2 (ibmgpu_stepper_distribute): over the context's NCCL ranks, or
         `virtual_ranks` emulated ranks on this GPU (0: back to the single-GPU solve)."""

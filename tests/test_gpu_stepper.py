@@ -100,3 +100,23 @@ def test_stepper_operators_match_golden():
     assert h.n_levels == len(gold["levels"])
     for l, gl in enumerate(gold["levels"]):
         assert H.csr_hash(H.dev_to_csr(h.level(l)["A"]))[0] == gl["A"]["struct"], l
+
+
+def test_vorticity_matches_diagnostics_formula():
+    """compute_vorticity (diagnostics.hpp:42-56) on the device == the same arithmetic on the
+    downloaded q, bit for bit."""
+    st = ibm.Stepper(H.case("cylinder_re40_smoke"))
+    for _ in range(3):
+        assert st.advance().ok
+    w = st.vorticity()
+    g, q = st.grid(), st.get("q")
+    nx, ny = st.nx, st.ny
+    n_u = (nx - 1) * ny
+    i = np.arange(1, nx)[None, :]
+    j = np.arange(1, ny)[:, None]
+    v = lambda ii, jf: n_u + ii + (jf - 1) * nx
+    u = lambda i_f, jj: (i_f - 1) + jj * (nx - 1)
+    dvdx = (q[v(i, j)] / g["dx"][i] - q[v(i - 1, j)] / g["dx"][i - 1]) / g["del_x"][i - 1]
+    dudy = (q[u(i, j)] / g["dy"][j] - q[u(i, j - 1)] / g["dy"][j - 1]) / g["del_y"][j - 1]
+    ref = (dvdx - dudy).ravel()
+    assert w.shape == ref.shape and np.array_equal(w, ref)
