@@ -349,7 +349,9 @@ void mat_plan_adaptive(Ctx* c, Mat* m) {
 void plan_adaptive_from(Ctx* c, Mat* m, const std::vector<int>& rp) {
     const double avg = m->rows ? double(m->nnz) / m->rows : 0.0;
     {
-        constexpr int kChunkNnz = 2048;
+        // ~2k nonzeros per CTA, but small matrices use smaller chunks so the grid still fills every
+        // SM (>= 4 CTAs each; 8 and 2 measured slower): these levels are latency-bound
+        const int kChunkNnz = std::clamp(static_cast<int>(m->nnz / std::max(1, c->num_sms * 4)), 512, 2048);
         // rows much longer than the mean never share a CTA with short rows
         const int kOwnCta = std::max(128, static_cast<int>(4.0 * avg));
         std::vector<int4> meta;
