@@ -11,6 +11,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "internal.cuh"
@@ -255,7 +256,12 @@ void mat_plan(Ctx* c, Mat* m) {
     m->max_row = d2h_scalar(c, mx.p);
     const double avg = m->rows ? double(m->nnz) / m->rows : 0.0;
     if (avg <= 12.0 && !std::getenv("IBMGPU_NO_STENCIL") && try_stencil(c, m)) return;
-    if (avg <= 12.0 && m->max_row <= 48) {
+    // Thread-per-row kernels pay one dependent load chain per row: on a small matrix (one short
+    // wave) a single long row sets the kernel time (S-4M L6 P^T: 1-entry rows plus a few of 86,
+    // 16 us). There, rows longer than max(16, 4 x mean) go to the warp-per-row path instead.
+    const bool small = m->rows < 65536;
+    const int kWide = small ? std::max(16, 4 * static_cast<int>(std::ceil(avg))) : 96;
+    if (avg <= 12.0 && m->max_row <= 48 && (!small || m->max_row <= kWide)) {
         m->kind = SPMV_SELL;
         m->sell_off.alloc(c, (size_t)n_slices + 1);
         exclusive_scan_total(c, width.p, m->sell_off.p, n_slices);
@@ -275,7 +281,7 @@ void mat_plan(Ctx* c, Mat* m) {
     // tail of the Galerkin levels: force unknowns couple to many aggregates) get a warp each with
     // an in-order sum, so one long row no longer sends the whole level to the adaptive kernel
     {
-        constexpr int kSigma = 512, kWide = 96;
+        constexpr int kSigma = 512;
         std::vector<int> shortrows, longrows;
         long long long_nnz = 0;
         for (int i = 0; i < m->rows; ++i) {
