@@ -14,6 +14,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <climits>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -26,7 +27,7 @@ namespace ibmgpu {
 
 namespace {
 
-constexpr long long kProductBudget = 1ll << 27;  // products per ESC chunk (~4.3 GB of sort buffers)
+constexpr long long kProductBudget = 1ll << 25;  // products per ESC chunk (~1.1 GB of sort buffers)
 
 __global__ void k_row_of(int rows, const int* __restrict__ rp, int* __restrict__ row_of) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -95,11 +96,32 @@ __global__ void k_seg_start(long long n, const int* __restrict__ head, const int
 __global__ void k_seg_sum(int n_unique, long long n, const long long* __restrict__ start,
                           const unsigned long long* __restrict__ keys, const double* __restrict__ vals,
                           int* __restrict__ ci, double* __restrict__ v, int* __restrict__ rowcnt) {
+    // thread per segment; segments longer than 64 products (the coarse body-tail entries sum
+    // thousands) are summed by the whole warp: 32 products in flight per load, added in order
+    // from shuffles — the same rounding sequence, without a serial load chain
     const int u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= n_unique) return;
-    const long long b = start[u], e = u + 1 < n_unique ? start[u + 1] : n;
+    const int lane = threadIdx.x & 31;
+    const bool valid = u < n_unique;
+    long long b = 0, e = 0;
+    if (valid) b = start[u], e = u + 1 < n_unique ? start[u + 1] : n;
+    const bool is_long = valid && e - b > 64;
     double s = 0.0;
-    for (long long p = b; p < e; ++p) s = addd(s, vals[p]);
+    if (valid && !is_long)
+        for (long long p = b; p < e; ++p) s = addd(s, vals[p]);
+    for (unsigned longs = __ballot_sync(kFull, is_long); longs; longs &= longs - 1) {
+        const int l = __ffs(longs) - 1;
+        const long long lb = __shfl_sync(kFull, b, l), le = __shfl_sync(kFull, e, l);
+        double acc = 0.0;
+        double x = lb + lane < le ? vals[lb + lane] : 0.0;
+        for (long long p0 = lb; p0 < le; p0 += 32) {
+            const double xn = p0 + 32 + lane < le ? vals[p0 + 32 + lane] : 0.0;
+            const int cnt = (int)min(32ll, le - p0);
+            for (int j = 0; j < cnt; ++j) acc = addd(acc, __shfl_sync(kFull, x, j));
+            x = xn;
+        }
+        if (lane == l) s = acc;
+    }
+    if (!valid) return;
     ci[u] = (int)(keys[b] & 0xffffffffu);
     v[u] = s;
     atomicAdd(rowcnt + (int)(keys[b] >> 32), 1);
@@ -433,6 +455,336 @@ __global__ void k_chunk_bounds(int rows, const long long* __restrict__ pref, lon
 // SpMV plans are built lazily (spmv / solver setup), not for every intermediate product.
 Mat* finish_plan(Ctx*, Mat* m) { return m; }
 
+// ---------------------------------------------------------------- hash SpGEMM (warp per row)
+// spmm_rows (sparse.hpp:226-268) with one warp per output row and the row's accumulator as an
+// open-addressing hash table in shared memory — instead of sorting every product. Products are
+// formed 32 at a time in Gustavson order (A-row entry, then B-row entry); lanes whose products hit
+// the same column are grouped with __match_any_sync and the group's first lane adds them to the
+// table entry in lane (= Gustavson) order, so each column's sum is 0.0 + p1 + p2 + ... exactly as
+// the reference accumulates it. Columns are then sorted (bitonic, in shared memory). Symbolic
+// pass: unique counts per row; a row over 3/4 of the symbolic table sends the product to ESC.
+constexpr int kHashSym = 4096, kSymWarps = 8;
+
+__device__ __forceinline__ unsigned hslot(int c, int mask) { return ((unsigned)c * 2654435761u) & (unsigned)mask; }
+
+// The 32 A entries of one chunk: B-row start, product offsets (inclusive scan), A value.
+struct HashChunk {
+    int off[33];
+    int bs[32];
+    double a[32];
+};
+
+__device__ __forceinline__ int chunk_load(HashChunk& ch, int c0, int e, const int* __restrict__ aci,
+                                          const double* __restrict__ av, const int* __restrict__ brp, int lane,
+                                          bool values) {
+    const int kk = c0 + lane;
+    int bs = 0, bl = 0;
+    double a = 0.0;
+    if (kk < e) {
+        const int k = __ldg(aci + kk);
+        bs = __ldg(brp + k);
+        bl = __ldg(brp + k + 1) - bs;
+        if (values) a = __ldg(av + kk);
+    }
+    int inc = bl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += t;
+    }
+    ch.off[lane + 1] = inc;
+    if (lane == 0) ch.off[0] = 0;
+    ch.bs[lane] = bs;
+    if (values) ch.a[lane] = a;
+    __syncwarp();
+    return __shfl_sync(kFull, inc, 31);
+}
+
+__device__ __forceinline__ int chunk_owner(const HashChunk& ch, int q) {  // largest o with off[o] <= q
+    int lo = 0, hi = 31;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (ch.off[mid] <= q)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kSymWarps * 32) k_hash_symbolic(int r0, int rows, const int* __restrict__ arp,
+                                                                  const int* __restrict__ aci,
+                                                                  const int* __restrict__ brp,
+                                                                  const int* __restrict__ bci, int* __restrict__ cnt,
+                                                                  int* __restrict__ maxcnt,
+                                                                  const long long* __restrict__ rprod,
+                                                                  long long limit) {
+    extern __shared__ int hsm[];
+    __shared__ HashChunk chunks[kSymWarps];
+    __shared__ int counter[kSymWarps];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int* keys = hsm + w * kHashSym;
+    HashChunk& ch = chunks[w];
+    for (int row = blockIdx.x * kSymWarps + w; row < rows; row += gridDim.x * kSymWarps) {
+        if (rprod[row] > limit) continue;  // long row: counted by the ESC pass
+        for (int t = lane; t < kHashSym; t += 32) keys[t] = -1;
+        if (lane == 0) counter[w] = 0;
+        __syncwarp();
+        const int i = r0 + row, b = __ldg(arp + i), e = __ldg(arp + i + 1);
+        for (int c0 = b; c0 < e; c0 += 32) {
+            if (*(volatile int*)(counter + w) > kHashSym * 3 / 4) break;  // overflow: ESC takes over
+            const int total = chunk_load(ch, c0, e, aci, nullptr, brp, lane, false);
+            for (int q0 = 0; q0 < total; q0 += 32) {
+                if (*(volatile int*)(counter + w) > kHashSym * 3 / 4) break;
+                const int q = q0 + lane;
+                if (q < total) {
+                    const int o = chunk_owner(ch, q);
+                    const int col = __ldg(bci + ch.bs[o] + (q - ch.off[o]));
+                    unsigned h = hslot(col, kHashSym - 1);
+                    for (int probe = 0; probe < kHashSym; ++probe) {
+                        const int prev = atomicCAS(keys + h, -1, col);
+                        if (prev == -1) {
+                            atomicAdd(counter + w, 1);
+                            break;
+                        }
+                        if (prev == col) break;
+                        h = (h + 1) & (kHashSym - 1);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        __syncwarp();
+        if (lane == 0) {
+            cnt[row] = counter[w];
+            atomicMax(maxcnt, counter[w]);
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void k_hash_numeric(int r0, int rows, const int* __restrict__ arp, const int* __restrict__ aci,
+                               const double* __restrict__ av, const int* __restrict__ brp,
+                               const int* __restrict__ bci, const double* __restrict__ bv,
+                               const int* __restrict__ crp, int* __restrict__ cci, double* __restrict__ cv,
+                               int slots, const long long* __restrict__ rprod, long long limit) {
+    extern __shared__ double hsd[];
+    const int nw = blockDim.x >> 5;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* vals = hsd + (size_t)w * slots;
+    int* keys = reinterpret_cast<int*>(hsd + (size_t)nw * slots) + (size_t)w * slots;
+    HashChunk* chunks = reinterpret_cast<HashChunk*>(reinterpret_cast<int*>(hsd + (size_t)nw * slots) + (size_t)nw * slots);
+    double* prod = reinterpret_cast<double*>(chunks + nw) + w * 32;
+    HashChunk& ch = chunks[w];
+    const int mask = slots - 1;
+    for (int row = blockIdx.x * nw + w; row < rows; row += gridDim.x * nw) {
+        if (rprod[row] > limit) continue;
+        for (int t = lane; t < slots; t += 32) {
+            keys[t] = -1;
+            vals[t] = 0.0;
+        }
+        __syncwarp();
+        const int i = r0 + row, b = __ldg(arp + i), e = __ldg(arp + i + 1);
+        for (int c0 = b; c0 < e; c0 += 32) {
+            const int total = chunk_load(ch, c0, e, aci, av, brp, lane, true);
+            for (int q0 = 0; q0 < total; q0 += 32) {
+                const int q = q0 + lane;
+                int col = -1;
+                double p = 0.0;
+                if (q < total) {
+                    const int o = chunk_owner(ch, q);
+                    const int jj = ch.bs[o] + (q - ch.off[o]);
+                    col = __ldg(bci + jj);
+                    p = mul(ch.a[o], __ldg(bv + jj));
+                }
+                prod[lane] = p;
+                const unsigned grp = __match_any_sync(kFull, col);
+                __syncwarp();
+                if (col >= 0 && lane == __ffs(grp) - 1) {
+                    unsigned h = hslot(col, mask);
+                    for (;;) {  // find or claim the column's slot (other leaders hold other columns)
+                        const int prev = atomicCAS(keys + h, -1, col);
+                        if (prev == -1 || prev == col) break;
+                        h = (h + 1) & mask;
+                    }
+                    double acc = vals[h];
+                    for (unsigned m = grp; m; m &= m - 1) acc = addd(acc, prod[__ffs(m) - 1]);
+                    vals[h] = acc;
+                }
+                __syncwarp();
+            }
+            __syncwarp();
+        }
+        // compact the occupied slots to the front (in slot order; positions never pass a read)
+        int n_u = 0;
+        for (int base = 0; base < slots; base += 32) {
+            const int t = base + lane;
+            const int k = keys[t];
+            const double v = vals[t];
+            const unsigned has = __ballot_sync(kFull, k != -1);
+            __syncwarp();
+            if (k != -1) {
+                const int pos = n_u + __popc(has & ((1u << lane) - 1));
+                keys[pos] = k;
+                vals[pos] = v;
+            }
+            n_u += __popc(has);
+            __syncwarp();
+        }
+        int n2 = 1;
+        while (n2 < n_u) n2 <<= 1;
+        for (int t = n_u + lane; t < n2; t += 32) keys[t] = INT_MAX;
+        __syncwarp();
+        for (int k = 2; k <= n2; k <<= 1)  // bitonic sort by column (columns are unique)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int t = lane; t < n2; t += 32) {
+                    const int u = t ^ j;
+                    if (u > t) {
+                        const int kt = keys[t], ku = keys[u];
+                        if ((kt > ku) == ((t & k) == 0)) {
+                            keys[t] = ku;
+                            keys[u] = kt;
+                            const double vt = vals[t];
+                            vals[t] = vals[u];
+                            vals[u] = vt;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        const int o0 = crp[row];
+        for (int t = lane; t < n_u; t += 32) {
+            cci[o0 + t] = keys[t];
+            cv[o0 + t] = vals[t];
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void k_long_flags(int n, const long long* __restrict__ rprod, long long limit, int* __restrict__ flag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) flag[i] = rprod[i] > limit;
+}
+__global__ void k_long_rows(int n, const int* __restrict__ flag, const int* __restrict__ pos, int r0,
+                            const int* __restrict__ arp, int* __restrict__ idx, int* __restrict__ len) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && flag[i]) {
+        idx[pos[i]] = i;
+        len[pos[i]] = arp[r0 + i + 1] - arp[r0 + i];
+    }
+}
+__global__ void k_gather_rows(int nl, const int* __restrict__ idx, int r0, const int* __restrict__ arp,
+                              const int* __restrict__ aci, const double* __restrict__ av,
+                              const int* __restrict__ lrp, int* __restrict__ lci, double* __restrict__ lv) {
+    const int r = blockIdx.x;
+    if (r >= nl) return;
+    const int src = arp[r0 + idx[r]], n = lrp[r + 1] - lrp[r];
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        lci[lrp[r] + k] = aci[src + k];
+        lv[lrp[r] + k] = av[src + k];
+    }
+}
+__global__ void k_long_counts(int nl, const int* __restrict__ idx, const int* __restrict__ crp_long,
+                              int* __restrict__ cnt) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < nl) cnt[idx[r]] = crp_long[r + 1] - crp_long[r];
+}
+__global__ void k_place_rows(int nl, const int* __restrict__ idx, const int* __restrict__ lrp,
+                             const int* __restrict__ lci, const double* __restrict__ lv, const int* __restrict__ crp,
+                             int* __restrict__ cci, double* __restrict__ cv) {
+    const int r = blockIdx.x;
+    if (r >= nl) return;
+    const int dst = crp[idx[r]], src = lrp[r], n = lrp[r + 1] - lrp[r];
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        cci[dst + k] = lci[src + k];
+        cv[dst + k] = lv[src + k];
+    }
+}
+
+Mat* esc_rows(Ctx* c, const Mat* A, int r0, int r1, const Mat* B);
+
+// Hash path for rows [r0, r1) of A*B (rprod: products per row). Rows of more than
+// kHashMaxProducts products — the few body-tail rows of the coarse Galerkin products reach
+// millions — are gathered into a side matrix and go through ESC, which spreads them over the
+// whole GPU; their results are placed back. nullptr if a short row's column count overflows.
+constexpr long long kHashMaxProducts = 1 << 17;
+Mat* spmm_hash(Ctx* c, const Mat* A, int r0, int r1, const Mat* B, const long long* rprod) {
+    const int rows = r1 - r0;
+    if (rows <= 0 || A->nnz == 0) return nullptr;
+    const bool prof = std::getenv("IBMGPU_SETUP_PROFILE") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what, long long extra) {
+        if (!prof) return;
+        sync(c);
+        const auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[hash] rows %d %-9s %8.3f ms (%lld)\n", rows, what,
+                     std::chrono::duration<double, std::milli>(t1 - t0).count(), extra);
+        t0 = t1;
+    };
+    const long long limit = kHashMaxProducts;
+    DBuf<int> cnt(c, (size_t)rows), mx(c, 1);
+    CK(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (size_t)rows, c->stream));
+    CK(cudaMemsetAsync(mx.p, 0, sizeof(int), c->stream));
+    // long rows -> side matrix -> ESC
+    DBuf<int> flag(c, (size_t)rows), pos(c, (size_t)rows + 1);
+    k_long_flags<<<blocks(rows), 256, 0, c->stream>>>(rows, rprod, limit, flag.p);
+    CK_LAUNCH(c);
+    exclusive_scan_total(c, flag.p, pos.p, rows);
+    const int nl = d2h_scalar(c, pos.p + rows);
+    DBuf<int> lidx;
+    Mat* Cl = nullptr;
+    if (nl > 0) {
+        lidx.alloc(c, (size_t)nl);
+        DBuf<int> llen(c, (size_t)nl);
+        k_long_rows<<<blocks(rows), 256, 0, c->stream>>>(rows, flag.p, pos.p, r0, A->rp.p, lidx.p, llen.p);
+        CK_LAUNCH(c);
+        Mat* Al = mat_new(c, nl, A->cols, 0);
+        exclusive_scan_total(c, llen.p, Al->rp.p, nl);
+        Al->nnz = d2h_scalar(c, Al->rp.p + nl);
+        Al->ci.alloc(c, (size_t)std::max(Al->nnz, 1));
+        Al->v.alloc(c, (size_t)std::max(Al->nnz, 1));
+        k_gather_rows<<<nl, 256, 0, c->stream>>>(nl, lidx.p, r0, A->rp.p, A->ci.p, A->v.p, Al->rp.p, Al->ci.p,
+                                                  Al->v.p);
+        CK_LAUNCH(c);
+        Cl = esc_rows(c, Al, 0, nl, B);
+        delete Al;
+        k_long_counts<<<blocks(nl), 256, 0, c->stream>>>(nl, lidx.p, Cl->rp.p, cnt.p);
+        CK_LAUNCH(c);
+    }
+    lap("long/ESC", nl);
+    std::unique_ptr<Mat> hold(Cl);
+    const size_t sym_smem = sizeof(int) * (size_t)kSymWarps * kHashSym;
+    CK(cudaFuncSetAttribute(k_hash_symbolic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem));
+    const int sgrid = std::min((rows + kSymWarps - 1) / kSymWarps, c->num_sms * 4);
+    k_hash_symbolic<<<sgrid, kSymWarps * 32, sym_smem, c->stream>>>(r0, rows, A->rp.p, A->ci.p, B->rp.p, B->ci.p,
+                                                                      cnt.p, mx.p, rprod, limit);
+    CK_LAUNCH(c);
+    const int maxc = d2h_scalar(c, mx.p);
+    lap("symbolic", maxc);
+    if (maxc > kHashSym * 3 / 4) return nullptr;
+    int slots = 64;
+    while (slots < 2 * maxc) slots <<= 1;
+    const size_t per_warp = (size_t)slots * (sizeof(double) + sizeof(int)) + sizeof(HashChunk) + 32 * sizeof(double);
+    const int nw = (int)std::max<size_t>(1, std::min<size_t>(8, (200u << 10) / per_warp));
+    const size_t smem = per_warp * nw;
+    Mat* m = mat_new(c, rows, B->cols, 0);
+    exclusive_scan_total(c, cnt.p, m->rp.p, rows);
+    m->nnz = d2h_scalar(c, m->rp.p + rows);
+    m->ci.alloc(c, (size_t)std::max(m->nnz, 1));
+    m->v.alloc(c, (size_t)std::max(m->nnz, 1));
+    CK(cudaFuncSetAttribute(k_hash_numeric, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int ngrid = std::min((rows + nw - 1) / nw, c->num_sms * 8);
+    k_hash_numeric<<<ngrid, nw * 32, smem, c->stream>>>(r0, rows, A->rp.p, A->ci.p, A->v.p, B->rp.p, B->ci.p, B->v.p,
+                                                        m->rp.p, m->ci.p, m->v.p, slots, rprod, limit);
+    CK_LAUNCH(c);
+    if (nl > 0) {
+        k_place_rows<<<nl, 256, 0, c->stream>>>(nl, lidx.p, Cl->rp.p, Cl->ci.p, Cl->v.p, m->rp.p, m->ci.p, m->v.p);
+        CK_LAUNCH(c);
+    }
+    lap("numeric", slots);
+    return m;
+}
+
 }  // namespace
 
 Mat* transpose(Ctx* c, const Mat* A) {
@@ -463,7 +815,19 @@ Mat* transpose(Ctx* c, const Mat* A) {
 
 Mat* spmm_rows(Ctx* c, const Mat* A, int r0, int r1, const Mat* B) {
     require(A->cols == B->rows, "spmm: dimension mismatch");
+    if (r1 > r0 && A->nnz > 0 && !std::getenv("IBMGPU_ESC_ONLY")) {
+        DBuf<long long> rprod(c, (size_t)(r1 - r0));
+        k_row_products<<<blocks(r1 - r0), 256, 0, c->stream>>>(r1 - r0, A->rp.p + r0, A->ci.p, B->rp.p, rprod.p);
+        CK_LAUNCH(c);
+        if (Mat* h = spmm_hash(c, A, r0, r1, B, rprod.p)) return finish_plan(c, h);
+    }
+    return esc_rows(c, A, r0, r1, B);
+}
+
+namespace {
+Mat* esc_rows(Ctx* c, const Mat* A, int r0, int r1, const Mat* B) {
     const int rows = r1 - r0;
+
     DBuf<int> row_of(c, (size_t)std::max(A->nnz, 1));
     if (A->nnz) {
         k_row_of<<<blocks(A->rows), 256, 0, c->stream>>>(A->rows, A->rp.p, row_of.p);
@@ -496,6 +860,7 @@ Mat* spmm_rows(Ctx* c, const Mat* A, int r0, int r1, const Mat* B) {
     if (parts.size() == 1) parts.clear();
     return finish_plan(c, out);
 }
+}  // namespace
 
 Mat* triple_product(Ctx* c, const Mat* A, const Mat* B, const Mat* C, int slice, long long* peak, int* slices) {
     require(A->cols == B->rows && B->cols == C->rows, "sliced_triple_product: dimension mismatch");
