@@ -358,6 +358,7 @@ def main():
                     help="N>1: row-slab distributed solve 2 over NCCL (one simulation), or N replicas")
     ap.add_argument("--min-dist-rows", type=int, default=200000,
                     help="SA levels with fewer rows are replicated on every rank")
+    ap.add_argument("--watchdog", type=float, default=900.0, help="N>1: abort after this many seconds")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -368,6 +369,14 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo", init_method="env://")
+        # A wedged collective must not hang the job: if the whole run has not finished within
+        # --watchdog seconds, this rank reports and exits (the other ranks' watchdogs do the same).
+        def _watchdog():
+            time.sleep(args.watchdog)
+            print(json.dumps({"error": f"rank {rank}: no completion within {args.watchdog}s (watchdog)"}),
+                  file=sys.stderr, flush=True)
+            os._exit(3)
+        threading.Thread(target=_watchdog, daemon=True).start()
     out, st = run_ours(args, rank, world)
     if world > 1:
         import torch
