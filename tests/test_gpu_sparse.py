@@ -143,3 +143,27 @@ def test_stencil_format_spmv_bitwise(port, ref, op):
     m = c.op(op)
     x = np.cos(np.arange(m.cols) * 0.61 + 0.2)
     assert np.array_equal(dev(m).spmv(x), port.spmv(m, x))
+
+
+def test_spmm_hash_and_long_row_paths_bitwise(port):
+    """Both SpGEMM paths against spmm_rows (sparse.hpp:226-268): rows averaging >= 32 products go
+    through the warp hash accumulator, and a row of more than 131k products through ESC (placed
+    back into the hash result). Gustavson-order sums, cancelled entries kept: bit-exact."""
+    rng = np.random.default_rng(17)
+    m, k, n = 60, 400, 500
+    ra, ca, va = [], [], []
+    for i in range(m):
+        cols = np.arange(k) if i == 7 else np.sort(rng.choice(k, 40, replace=False))
+        ra += [i] * len(cols)
+        ca += cols.tolist()
+        va += rng.uniform(-1, 1, len(cols)).tolist()
+    rb, cb, vb = [], [], []
+    for i in range(k):
+        cols = np.sort(rng.choice(n, 420, replace=False))
+        rb += [i] * len(cols)
+        cb += cols.tolist()
+        vb += rng.choice([-1.0, 1.0, 0.5, -0.5], len(cols)).tolist()  # exact cancellations occur
+    A = port.from_triplets(m, k, np.array(ra), np.array(ca), np.array(va))
+    B = port.from_triplets(k, n, np.array(rb), np.array(cb), np.array(vb))
+    C = ibm.spmm(dev(A), dev(B))
+    H.assert_csr_equal(H.dev_to_csr(C), port.spmm(A, B))
