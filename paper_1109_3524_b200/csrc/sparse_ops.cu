@@ -172,9 +172,7 @@ __global__ void k_pin_rows(int rows, int pin, const int* __restrict__ rp, const 
             ov[o] = 1.0;
         }
         n = 1;
-    } else {
-        bool placed = false;  // (pin,pin) only lives in row pin
-        (void)placed;
+    } else {  // (pin, pin) only lives in row pin
         for (int k = rp[i]; k < rp[i + 1]; ++k) {
             const int c = ci[k];
             if (c == pin || v[k] == 0.0) continue;
