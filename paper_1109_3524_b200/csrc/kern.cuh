@@ -279,21 +279,38 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_stencil(int rows, StencilPla
     const int i = blockIdx.x * kBlock + threadIdx.x;
     const bool live = i < rows;
     // mask and band values are constant for the solve: loaded before griddepcontrol.wait
+    // With a single stride (lhs2) nothing waits on the mask byte: the five band values (stored 0.0
+    // where a slot is absent) and the five x gathers (indices clamped into range) all issue at
+    // once; the mask only selects which products enter the column-order sum. With two strides
+    // (velocity A / L: u and v blocks) the stride comes from the mask.
+    const bool one_stride = P.S2 == 0;
     const unsigned m = live ? __ldg(P.mask + i) : 0u;
-    const int S = (m & 64u) ? P.S2 : P.S1;
     double a[5], xv[5];
-    const int col[5] = {i - S, i - 1, i, i + 1, i + S};
+    if (one_stride) {
 #pragma unroll
-    for (int q = 0; q < 5; ++q)
-        if (m & (1u << q)) a[q] = __ldg(P.v + (size_t)q * rows + i);
+        for (int q = 0; q < 5; ++q) a[q] = live ? __ldg(P.v + (size_t)q * rows + i) : 0.0;
+    } else {
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+            if (m & (1u << q)) a[q] = __ldg(P.v + (size_t)q * rows + i);
+    }
     pdl_wait();
     if (epi.skip()) return;
     if constexpr (requires { epi.touch(0); }) {
         if (live) epi.touch(i);
     }
+    if (one_stride) {
+        const int S = P.S1, ic = live ? i : 0;
+        const int col[5] = {max(ic - S, 0), max(ic - 1, 0), ic, min(ic + 1, rows - 1), min(ic + S, rows - 1)};
 #pragma unroll
-    for (int q = 0; q < 5; ++q)
-        if (m & (1u << q)) xv[q] = xf(col[q]);
+        for (int q = 0; q < 5; ++q) xv[q] = xf(col[q]);
+    } else {
+        const int S = (m & 64u) ? P.S2 : P.S1;
+        const int col[5] = {i - S, i - 1, i, i + 1, i + S};
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+            if (m & (1u << q)) xv[q] = xf(col[q]);
+    }
     double s = 0.0;
 #pragma unroll
     for (int q = 0; q < 5; ++q)
