@@ -442,13 +442,15 @@ struct ibmgpu_stepper {
 
     // row-slab solve 2 (dist.cu): enabled by ibmgpu_stepper_distribute
     int dist_ranks = 0, dist_min_rows = 0;
-    Dist* dist = nullptr;
+    Dist* dist = nullptr;   // solve 2 (SA)
+    Dist* dist1 = nullptr;  // solve 1 (diagonal); A never changes, so planned once
     bool dist_stale = true;
-    DBuf<double> b2, x2;
+    DBuf<double> b2, x2, b1, x1;
 
     ~ibmgpu_stepper() {
         if (c) cudaStreamSynchronize(c->stream);
         dist_destroy(dist);
+        dist_destroy(dist1);
         if (c) {
             pcg_forget(c, A, nullptr);
             pcg_forget(c, lhs2, hier);
@@ -525,6 +527,26 @@ struct ibmgpu_stepper {
                 cj.push_back(std::clamp(j, 0, g.ny - 1));
             }
         return ibmhost::partition_lambda(g.nx, g.ny, n_b, cj.data(), R);
+    }
+
+    // row owners of q: u(i_f, j) with the slab of cell row j, v(i, j_f) with the slab of j_f
+    std::vector<int> q_owner(int R) const {
+        std::vector<int> own((size_t)n_q);
+        auto slab = [&](int j) { return static_cast<int>((static_cast<long long>(std::clamp(j, 0, g.ny - 1)) * R) / g.ny); };
+        for (int j = 0; j < g.ny; ++j)
+            for (int i_f = 1; i_f < g.nx; ++i_f) own[(size_t)g.u_id(i_f, j)] = slab(j);
+        for (int j_f = 1; j_f < g.ny; ++j_f)
+            for (int i = 0; i < g.nx; ++i) own[(size_t)g.v_id(i, j_f)] = slab(j_f);
+        return own;
+    }
+
+    void ensure_dist1() {
+        if (dist1) return;
+        const int R = c->nccl ? c->nranks : dist_ranks;
+        const auto own = q_owner(R);
+        dist1 = dist_create(c, A, IBMGPU_PC_DIAGONAL, nullptr, own.data(), c->nccl ? 1 : dist_ranks, 0);
+        b1.alloc(c, (size_t)n_q);
+        x1.alloc(c, (size_t)n_q);
     }
 
     void ensure_dist() {
@@ -809,18 +831,27 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
                                                    S->bnd_n.p, S->bnd.p, S->bcn.p, S->bcnp1.p);
         CK_LAUNCH(c);
     }
-    PcgPlan* P1 = pcg_plan(c, S->A, IBMGPU_PC_DIAGONAL, nullptr);
+    // stage 1 (single GPU: one graph launch; distributed: row-slab PCG-diag over q slabs)
+    const bool distributed = S->dist_ranks > 0 || c->nccl != nullptr;
+    if (distributed) S->ensure_dist1();
+    PcgPlan* P1 = distributed ? nullptr : pcg_plan(c, S->A, IBMGPU_PC_DIAGONAL, nullptr);
+    double* b1 = distributed ? S->b1.p : P1->b.p;
+    double* qs = distributed ? S->x1.p : P1->x.p;  // q* after the solve (full on every rank)
     const double c1 = S->have_conv ? 1.5 : 1.0, c2 = S->have_conv ? 0.5 : 0.0;
     launch_spmv(c, S->L, XPlain{S->q.p},
-                EpiRhs1{S->mdt.p, S->q.p, S->bcn.p, S->bcnp1.p, S->conv.p, S->conv_prev.p, 0.5 * S->nu, c1, c2,
-                        P1->b.p, P1->x.p},
+                EpiRhs1{S->mdt.p, S->q.p, S->bcn.p, S->bcnp1.p, S->conv.p, S->conv_prev.p, 0.5 * S->nu, c1, c2, b1,
+                        qs},
                 s);
     CK(cudaEventRecord(S->ev[1], s));
-    // stage 1
-    P1->run(c, S->p1, nullptr);
-    CK(cudaEventRecord(S->ev[2], s));
     ibm_solve_result r1;
-    P1->finish(c, &r1);
+    if (distributed) {
+        dist_solve(S->dist1, b1, qs, S->p1, &r1, nullptr);
+        CK(cudaEventRecord(S->ev[2], s));
+    } else {
+        P1->run(c, S->p1, nullptr);
+        CK(cudaEventRecord(S->ev[2], s));
+        P1->finish(c, &r1);
+    }
     if (d2h_scalar(c, &S->sd.p->bc_err))
         fail(IBMGPU_ECUDA, "boundary: prescribed velocities have nonzero net flux and no convective edge to absorb it");
     rep->solve1_iters = r1.iterations;
@@ -832,13 +863,12 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
         return;
     }
     // stage 2 (single GPU: one graph launch; distributed: row-slab PCG, dist.cu)
-    const bool distributed = S->dist_ranks > 0 || c->nccl != nullptr;
     if (distributed) S->ensure_dist();
     PcgPlan* P2 = distributed ? nullptr : pcg_plan(c, S->lhs2, IBMGPU_PC_SA, S->hier);
     double* b2 = distributed ? S->b2.p : P2->b.p;
     double* lam = distributed ? S->x2.p : P2->x.p;
     const Bc2 bc2{S->bl, S->bnd.p, S->dx.p, S->dy.p};
-    launch_spmv(c, S->QT, XPlain{P1->x.p}, EpiRhs2{bc2, n_p, 0, S->ub.p, b2}, s);
+    launch_spmv(c, S->QT, XPlain{qs}, EpiRhs2{bc2, n_p, 0, S->ub.p, b2}, s);
     d2d(c, lam, S->lambda.p, (size_t)S->n_lambda);
     CK(cudaEventRecord(S->ev[3], s));
     ibm_solve_result r2;
@@ -858,10 +888,10 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
     }
     // stage 3: projection q = q* - B^N (Q lambda)
     if (S->bn_diagonal) {
-        launch_spmv(c, S->Q, XPlain{lam}, EpiProjectDiag{P1->x.p, S->bn_diag.p, S->q_new.p, &S->sd.p->nonfinite}, s);
+        launch_spmv(c, S->Q, XPlain{lam}, EpiProjectDiag{qs, S->bn_diag.p, S->q_new.p, &S->sd.p->nonfinite}, s);
     } else {
         launch_spmv(c, S->Q, XPlain{lam}, EpiStore{S->y.p}, s);
-        launch_spmv(c, S->BN, XPlain{S->y.p}, EpiProjectGen{P1->x.p, S->q_new.p, &S->sd.p->nonfinite}, s);
+        launch_spmv(c, S->BN, XPlain{S->y.p}, EpiProjectGen{qs, S->q_new.p, &S->sd.p->nonfinite}, s);
     }
     CK(cudaEventRecord(S->ev[5], s));
     launch_spmv(c, S->QT, XPlain{S->q_new.p},
@@ -1106,8 +1136,13 @@ int ibmgpu_stepper_distribute(ibmgpu_stepper_t S, int virtual_ranks, int min_dis
         S->dist_min_rows = min_dist_rows;
         S->dist_stale = true;
         dist_destroy(S->dist);
+        dist_destroy(S->dist1);
         S->dist = nullptr;
-        if (S->dist_ranks > 0) S->ensure_dist();
+        S->dist1 = nullptr;
+        if (S->dist_ranks > 0) {
+            S->ensure_dist1();
+            S->ensure_dist();
+        }
     });
 }
 

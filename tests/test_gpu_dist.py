@@ -116,15 +116,15 @@ def test_loopback_full_size_c2():
 
 @pytest.mark.parametrize("name,steps", [("cylinder_re40_smoke", 3), ("flapping_smoke", 3), ("cavity", 2)])
 def test_distributed_stepper_matches_single(name, steps):
-    """Stepper with solve 2 row-slab distributed over 3 emulated ranks vs the single-GPU stepper
-    (moving bodies re-plan every step)."""
+    """Stepper with both solves row-slab distributed over 3 emulated ranks vs the single-GPU stepper
+    (moving bodies re-plan solve 2 every step)."""
     a = ibm.Stepper(H.case(name))
     b = ibm.Stepper(H.case(name))
     b.distribute(virtual_ranks=3, min_dist_rows=0)
     for _ in range(steps):
         ra, rb = a.advance(), b.advance()
         assert ra.ok and rb.ok, (ra.message, rb.message)
-        assert abs(ra.solve2_iters - rb.solve2_iters) <= 2 and ra.solve1_iters == rb.solve1_iters
+        assert abs(ra.solve2_iters - rb.solve2_iters) <= 2 and abs(ra.solve1_iters - rb.solve1_iters) <= 2
     qa, qb = a.get("q"), b.get("q")
     la, lb = a.get("lambda"), b.get("lambda")
     assert np.linalg.norm(qa - qb) <= 1e-6 * np.linalg.norm(qa)

@@ -4,7 +4,8 @@ For a workload's coupled system (bench_rhs of runner.hpp) it times, on the devic
   single   ibmgpu_pcg (one conditional-graph launch)
   dist R   ibmgpu_dist_pcg with R emulated ranks (one graph launch per iteration, halos by D2D copy)
 Loopback runs every rank's kernels back to back on this GPU, so time/R approximates one rank's
-compute share when the R slabs run on R GPUs (communication not included). Prints JSON.
+compute share when the R slabs run on R GPUs (communication not included; the loopback halo copies
+are). b and x stay on the device; nothing crosses PCIe inside the timed region. Prints JSON.
 
   python tools/dist_bench.py [--workload c2|s4m|c5-N] [--ranks 1,2,4,8] [--min-dist-rows 200000]
 """
@@ -58,8 +59,18 @@ def main():
             best = min(best, ctx.timer_stop())
         return best, res
 
+    import ctypes as C
+    from paper_1109_3524_b200._lib import SolveResultC
+    lib = ctx.lib
+    pc = ibm.SolverParams().c()
+
+    # Device-resident solves: b stays on the device; x0 = 0 is a fresh device allocation (device
+    # memset); no host transfer inside the timed region.
     def single():
-        return ibm.pcg(A, bd, None, M, ibm.SolverParams())
+        x = ibm.DeviceVector(n, ctx)
+        res = SolveResultC()
+        ctx.check(lib.ibmgpu_pcg(ctx.h, A.h, M.kind, M.hier.h, bd.p, x.p, C.byref(pc), C.byref(res), None))
+        return res
 
     ms, r = timed(single)
     out["results"].append({"mode": "single", "ms": round(ms, 3), "iters": r.iterations,
@@ -70,7 +81,13 @@ def main():
         t0 = time.time()
         ds = ibm.DistSolver(A, M, owner, virtual_ranks=R, min_dist_rows=a.min_dist_rows)
         setup = time.time() - t0
-        ms, r = timed(lambda: ds.solve(bd))
+        def dist_solve():
+            x = ibm.DeviceVector(n, ctx)
+            res = SolveResultC()
+            ctx.check(lib.ibmgpu_dist_pcg(ds.h, bd.p, x.p, C.byref(pc), C.byref(res), None))
+            return res
+
+        ms, r = timed(dist_solve)
         info = ds.info()
         out["results"].append({"mode": f"loopback R={R}", "ms": round(ms, 3), "iters": r.iterations,
                                "ms_per_iter": round(ms / r.iterations, 4),
