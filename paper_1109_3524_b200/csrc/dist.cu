@@ -421,6 +421,10 @@ void exchange(Dist* d, GetM gm, GetV gv) {
     }
     if (d->R == 1) return;
     if (d->loop) {
+        // IBMGPU_DIST_NOCOPY=1 (timing experiments only, results are wrong): skip the loopback halo
+        // copies to separate their cost from the ranks' own work
+        static const bool nocopy = std::getenv("IBMGPU_DIST_NOCOPY") != nullptr;
+        if (nocopy) return;
         for (int r = 0; r < d->R; ++r) {
             DMat& Mr = gm(*d->ranks[r]);
             double* dst = gv(*d->ranks[r]) + Mr.n_own;

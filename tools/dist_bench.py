@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--ranks", default="1,2,4,8")
     ap.add_argument("--min-dist-rows", type=int, default=200000)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--iters", type=int, default=0, help="force exactly this many iterations (timing only)")
     a = ap.parse_args()
     cfg, h_min, dt, desc = workload(a.workload)
     st = ibm.Stepper(os.path.join(CASES, cfg + ".cfg"), h_min=h_min, dt=dt)
@@ -62,7 +63,7 @@ def main():
     import ctypes as C
     from paper_1109_3524_b200._lib import SolveResultC
     lib = ctx.lib
-    pc = ibm.SolverParams().c()
+    pc = (ibm.SolverParams(rel_tol=1e-30, max_iters=a.iters) if a.iters else ibm.SolverParams()).c()
 
     # Device-resident solves: b stays on the device; x0 = 0 is a fresh device allocation (device
     # memset); no host transfer inside the timed region.
