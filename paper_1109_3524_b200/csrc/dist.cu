@@ -395,6 +395,7 @@ struct ibmgpu_dist {
     ibmgpu::DBuf<double> gather_buf;                       // NCCL: R * max_own
     int max_own = 0;
     cudaGraphExec_t iter_exec = nullptr;                   // one captured PCG iteration
+    bool no_graph = false;                                 // capture failed: eager iterations
     int iter_kernels = 0;
     int* done_host = nullptr;                              // pinned, 2 slots
     cudaEvent_t ev[2] = {};
@@ -606,9 +607,17 @@ void enqueue_iteration(Dist* d) {
 void capture_iteration(Dist* d) {
     Ctx* c = d->c;
     const long long l0 = c->launches;
-    cudaGraph_t g;
+    cudaGraph_t g = nullptr;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    enqueue_iteration(d);
+    try {
+        enqueue_iteration(d);
+    } catch (...) {  // leave the stream usable: end (and drop) the broken capture
+        cudaStreamEndCapture(c->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        c->launches = l0;
+        throw;
+    }
     CK(cudaStreamEndCapture(c->stream, &g));
     CK(cudaGraphInstantiate(&d->iter_exec, g, 0));
     CK(cudaGraphDestroy(g));
@@ -822,7 +831,14 @@ void dist_solve(Dist* d, const double* b_full, double* x_full, const ibm_solver_
     CK(cudaMemcpyAsync(H0, d->ranks[0]->st.p, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
     sync(c);
     if (!H0->done) {
-        if (c->eager) {
+        if (!c->eager && !d->iter_exec && !d->no_graph) {
+            try {
+                capture_iteration(d);
+            } catch (const Error&) {
+                d->no_graph = true;  // e.g. a communicator that cannot be captured: run eagerly
+            }
+        }
+        if (c->eager || d->no_graph) {
             // profiling mode (IBMGPU_EAGER=1): kernels launched from the host, checked every iteration
             for (;;) {
                 enqueue_iteration(d);
@@ -834,7 +850,6 @@ void dist_solve(Dist* d, const double* b_full, double* x_full, const ibm_solver_
             // one graph launch per iteration (NCCL calls captured with the kernels); the done flag
             // of iteration k is read while iteration k+1 is already queued, so the GPU never idles
             // on the host check — the extra iteration's kernels see `done` and exit at once
-            if (!d->iter_exec) capture_iteration(d);
             const int* done_dev = &d->ranks[0]->st.p->done;
             for (int k = 0;; ++k) {
                 CK(cudaGraphLaunch(d->iter_exec, s));
