@@ -76,3 +76,25 @@ def test_first_step_matches_reference(case):
     assert abs(np.linalg.norm(st.get("q")) - s0["qn"]) <= 1e-6 * s0["qn"]
     assert abs(np.linalg.norm(st.get("lambda")) - s0["ln"]) <= 1e-6 * s0["ln"]
     assert r.div_residual <= 10 * 1e-5 and r.noslip_residual <= 10 * 1e-5
+
+
+def test_c2_first_step_tight_tolerance_matches_reference(ref, tmp_path):
+    """C2 at full size (1042^2, 1.09M-row lhs2) with both solvers at rel_tol 1e-10: one device
+    step against one step of the unmodified reference — fields agree far below the 1e-6 contract,
+    so the default-tolerance differences are solver noise, not discrepancies."""
+    name, h, dt = CFG["c2"]
+    cfg = open(H.case(name)).read()
+    cfg += "[solver1]\ntype = pcg-diag\nrel_tol = 1e-10\n[solver2]\ntype = pcg-sa\nrel_tol = 1e-10\n"
+    path = tmp_path / "c2_tight.cfg"
+    path.write_text(cfg)
+    rc = ref.case(str(path), h, dt)
+    st = ibm.Stepper(str(path), h_min=h, dt=dt)
+    r_ref = rc.step()
+    r = st.advance()
+    assert r.ok and bool(r_ref["ok"])
+    assert abs(r.solve2_iters - r_ref["solve2_iters"]) <= 2
+    assert H.rel_err(st.get("q"), rc.state("q")) <= 1e-9
+    lam, lr = st.get("lambda"), rc.state("lambda")
+    assert H.rel_err(lam[:st.n_p], lr[:st.n_p]) <= 1e-8
+    f, fr = st.forces(), rc.forces()
+    assert abs(f["cd"] - fr["cd"]) <= 1e-8 * abs(fr["cd"])
