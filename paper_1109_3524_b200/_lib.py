@@ -11,7 +11,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libibmgpu.so")
+# IBMGPU_LIB: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("IBMGPU_LIB") or os.path.join(HERE, "libibmgpu.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "ibmgpu.h")
 
 IBMGPU_OK, IBMGPU_EINVAL, IBMGPU_ESUPPORT, IBMGPU_ECUDA, IBMGPU_ENCCL, IBMGPU_ENOMEM = range(6)

@@ -359,15 +359,18 @@ __device__ __forceinline__ double row_sum_inorder(int row, const int* __restrict
     return s;
 }
 
-template <class XF, class Epi>
-__global__ void __launch_bounds__(kBlock, 4) k_spmv_sellw(int rows, const int* __restrict__ rp,
+// kU entries per software-pipeline stage. A matrix with few rows (every row a thread, < ~1000
+// threads per SM) cannot hide DRAM latency with more warps, only with more loads in flight per
+// thread: those launch the kU = 8 instance (its registers do not matter at that occupancy).
+template <class XF, class Epi, int kU = 4>
+__global__ void __launch_bounds__(kBlock, kU == 4 ? 4 : 2) k_spmv_sellw(int rows, const int* __restrict__ rp,
                                                           const int* __restrict__ perm, const int* __restrict__ off,
                                                           const int* __restrict__ ci, const double* __restrict__ v,
                                                           XF xf, Epi epi, int sblocks, const int* __restrict__ long_rows,
                                                           int n_long, const int* __restrict__ csr_ci,
                                                           const double* __restrict__ csr_v) {
     constexpr int NR = Epi::NR;
-    constexpr int U = 4;
+    constexpr int U = kU;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
@@ -564,9 +567,14 @@ inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
     } else if (A->kind == SPMV_SELLW) {
         const int sb = (A->n_short + kBlock - 1) / kBlock;
         grid = sb + (A->n_long + kBlock / 32 - 1) / (kBlock / 32);
-        launch_k(c, k_spmv_sellw<XF, Epi>, grid, kBlock, s, A->n_short, A->rp.p, A->perm.p, A->sell_off.p,
-                 A->sell_ci.p, A->sell_v.p, xf, epi, sb, (const int*)A->long_rows.p, A->n_long, (const int*)A->ci.p,
-                 (const double*)A->v.p);
+        if (A->n_short < c->num_sms * 1024 && A->nnz >= 40ll * A->rows)  // few, long rows
+            launch_k(c, k_spmv_sellw<XF, Epi, 8>, grid, kBlock, s, A->n_short, A->rp.p, A->perm.p, A->sell_off.p,
+                     A->sell_ci.p, A->sell_v.p, xf, epi, sb, (const int*)A->long_rows.p, A->n_long,
+                     (const int*)A->ci.p, (const double*)A->v.p);
+        else
+            launch_k(c, k_spmv_sellw<XF, Epi, 4>, grid, kBlock, s, A->n_short, A->rp.p, A->perm.p, A->sell_off.p,
+                     A->sell_ci.p, A->sell_v.p, xf, epi, sb, (const int*)A->long_rows.p, A->n_long,
+                     (const int*)A->ci.p, (const double*)A->v.p);
     } else {
         const AdaptPlan pl{A->blk_meta.p, A->lrow.p, A->lpart.p, A->lcnt.p};
         grid = A->n_blocks;
