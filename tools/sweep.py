@@ -1,0 +1,84 @@
+"""BASELINE metric "CG iters/sec vs grid size; SpMV HBM GB/s vs 8 TB/s" on the synthetic uniform
+cylinder grids (BASELINE configs[4], C5-N: N^2 cells): for each N, one SA-PCG solve of the coupled
+system on the runner.hpp bench right-hand side (device-resident b and x) and a timed lhs2 SpMV,
+plus two Stepper::advance steps (steps/s). One JSON line per grid.
+
+  python tools/sweep.py --sizes 1024,2048,4096,8192
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+from paper_1109_3524_b200 import ibm  # noqa: E402
+from paper_1109_3524_b200._lib import SolveResultC  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes", default="1024,2048,4096,8192")
+    ap.add_argument("--spmv-reps", type=int, default=20)
+    a = ap.parse_args()
+    peak, kind = bench.load_peaks()
+    for N in (int(s) for s in a.sizes.split(",")):
+        cfg, h, dt, desc = bench.workload(f"c5-{N}")
+        t0 = time.time()
+        st = ibm.Stepper(os.path.join(ROOT, "cases", cfg + ".cfg"), h_min=h, dt=dt)
+        setup = time.time() - t0
+        ctx, A = st.ctx, st.op("lhs2")
+        n = A.rows()
+        w = np.sin(0.7 * np.arange(n) + 0.3)
+        w[0] = 0.0
+        w /= np.linalg.norm(w)
+        b = ibm.DeviceVector.from_host(A.spmv(w), ctx)
+        M = ibm.SaPreconditioner(st.hierarchy())
+        pc = ibm.SolverParams().c()
+
+        def solve():
+            x = ibm.DeviceVector(n, ctx)
+            res = SolveResultC()
+            ctx.check(ctx.lib.ibmgpu_pcg(ctx.h, A.h, M.kind, M.hier.h, b.p, x.p, C.byref(pc), C.byref(res), None))
+            return res
+
+        solve()
+        ctx.sync()
+        ctx.timer_start()
+        r = solve()
+        ms = ctx.timer_stop()
+        b_it2, _ = bench.hier_bytes(st.hierarchy())
+        x = ibm.DeviceVector(n, ctx)
+        y = ibm.DeviceVector(n, ctx)
+        A.spmv_into(x, y)
+        ctx.sync()
+        ctx.timer_start()
+        for _ in range(a.spmv_reps):
+            A.spmv_into(x, y)
+        spmv_ms = ctx.timer_stop() / a.spmv_reps
+        sb = bench.spmv_bytes(n, n, A.nnz())
+        st.advance()
+        ctx.sync()
+        ctx.timer_start()
+        reps = [st.advance() for _ in range(2)]
+        step_ms = ctx.timer_stop() / 2
+        it_ms = ms / max(r.iterations, 1)
+        print(json.dumps({
+            "grid": f"{N}^2", "cells": N * N, "n_lambda": n, "nnz_lhs2": A.nnz(), "setup_s": round(setup, 2),
+            "cg_iters": r.iterations, "cg_iteration_ms": round(it_ms, 4),
+            "cg_iters_per_s": round(1e3 / it_ms, 1),
+            "cg_hbm_gbs": round(b_it2 / (it_ms * 1e-3) / 1e9, 1), "cg_frac_measured": round(b_it2 / (it_ms * 1e-3) / 1e9 / peak, 4),
+            "spmv_lhs2_us": round(spmv_ms * 1e3, 1), "spmv_hbm_gbs": round(sb / (spmv_ms * 1e-3) / 1e9, 1),
+            "spmv_frac_of_8tbs": round(sb / (spmv_ms * 1e-3) / 8e12, 4),
+            "steps_per_s": round(1e3 / step_ms, 3), "solve2_iters_per_step": [rr.solve2_iters for rr in reps],
+            "peak_kind": kind}), flush=True)
+        del st
+
+
+if __name__ == "__main__":
+    main()
