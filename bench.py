@@ -354,6 +354,7 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-s4m", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C5 grid-size sweep (1024^2..4096^2)")
     ap.add_argument("--parallel", default="slab", choices=["slab", "replicas"],
                     help="N>1: row-slab distributed solve 2 over NCCL (one simulation), or N replicas")
     ap.add_argument("--min-dist-rows", type=int, default=200000,
@@ -396,6 +397,15 @@ def main():
                 out["s4m"] = s4m_probe(args)
             except Exception as e:  # report, never hide
                 out["s4m"] = {"error": str(e)}
+        if not args.no_sweep and world == 1 and args.workload == "c2":
+            try:  # BASELINE metric "CG iters/sec vs grid size" (configs[4] synthetic grids)
+                sys.path.insert(0, os.path.join(ROOT, "tools"))
+                import sweep as _sweep
+                out["grid_sweep"] = [{k: r[k] for k in ("grid", "cg_iters_per_s", "cg_iteration_ms", "cg_frac_measured",
+                                                        "spmv_hbm_gbs", "steps_per_s")}
+                                     for r in _sweep.sweep([1024, 2048, 4096], spmv_reps=10)]
+            except Exception as e:
+                out["grid_sweep"] = {"error": str(e)}
         if not args.no_cpu and world == 1:
             try:
                 out["cpu_baseline"] = cpu_baseline(args)

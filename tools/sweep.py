@@ -21,13 +21,11 @@ from paper_1109_3524_b200 import ibm  # noqa: E402
 from paper_1109_3524_b200._lib import SolveResultC  # noqa: E402
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--sizes", default="1024,2048,4096,8192")
-    ap.add_argument("--spmv-reps", type=int, default=20)
-    a = ap.parse_args()
+def sweep(sizes, spmv_reps=20, emit=None):
+    """One record per C5-N grid (see module doc); emit(record) is called as each finishes."""
     peak, kind = bench.load_peaks()
-    for N in (int(s) for s in a.sizes.split(",")):
+    out = []
+    for N in sizes:
         cfg, h, dt, desc = bench.workload(f"c5-{N}")
         t0 = time.time()
         st = ibm.Stepper(os.path.join(ROOT, "cases", cfg + ".cfg"), h_min=h, dt=dt)
@@ -58,9 +56,9 @@ def main():
         A.spmv_into(x, y)
         ctx.sync()
         ctx.timer_start()
-        for _ in range(a.spmv_reps):
+        for _ in range(spmv_reps):
             A.spmv_into(x, y)
-        spmv_ms = ctx.timer_stop() / a.spmv_reps
+        spmv_ms = ctx.timer_stop() / spmv_reps
         sb = bench.spmv_bytes(n, n, A.nnz())
         st.advance()
         ctx.sync()
@@ -68,7 +66,7 @@ def main():
         reps = [st.advance() for _ in range(2)]
         step_ms = ctx.timer_stop() / 2
         it_ms = ms / max(r.iterations, 1)
-        print(json.dumps({
+        rec = {
             "grid": f"{N}^2", "cells": N * N, "n_lambda": n, "nnz_lhs2": A.nnz(), "setup_s": round(setup, 2),
             "cg_iters": r.iterations, "cg_iteration_ms": round(it_ms, 4),
             "cg_iters_per_s": round(1e3 / it_ms, 1),
@@ -76,8 +74,20 @@ def main():
             "spmv_lhs2_us": round(spmv_ms * 1e3, 1), "spmv_hbm_gbs": round(sb / (spmv_ms * 1e-3) / 1e9, 1),
             "spmv_frac_of_8tbs": round(sb / (spmv_ms * 1e-3) / 8e12, 4),
             "steps_per_s": round(1e3 / step_ms, 3), "solve2_iters_per_step": [rr.solve2_iters for rr in reps],
-            "peak_kind": kind}), flush=True)
+            "peak_kind": kind}
+        out.append(rec)
+        if emit:
+            emit(rec)
         del st
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--sizes", default="1024,2048,4096,8192")
+    ap.add_argument("--spmv-reps", type=int, default=20)
+    a = ap.parse_args()
+    sweep([int(s) for s in a.sizes.split(",")], a.spmv_reps, emit=lambda r: print(json.dumps(r), flush=True))
 
 
 if __name__ == "__main__":
