@@ -394,6 +394,10 @@ class Ref:
         L.ref_case_bodies.argtypes = [vp, _dp, _dp, _dp, _dp, _dp]
         L.ref_case_step.restype = C.c_int
         L.ref_case_step.argtypes = [vp, _dp, C.c_char_p, C.c_int]
+        L.ref_case_write_checkpoint.restype = C.c_int
+        L.ref_case_write_checkpoint.argtypes = [vp, C.c_char_p]
+        L.ref_case_read_checkpoint.restype = C.c_int
+        L.ref_case_read_checkpoint.argtypes = [vp, C.c_char_p]
         L.ref_case_state.restype = C.c_int
         L.ref_case_state.argtypes = [vp, C.c_int, _dp]
         L.ref_case_time.restype = C.c_double
@@ -633,6 +637,16 @@ class RefCase:
         out = {k: np.zeros(self.n_b) for k in ("x", "y", "ub_x", "ub_y", "ds")}
         self.ref.L.ref_case_bodies(self.h, *[_d(out[k]) for k in ("x", "y", "ub_x", "ub_y", "ds")])
         return out
+
+    def write_checkpoint(self, path: str):
+        """io.hpp:89-110 write_checkpoint of the reference Stepper."""
+        if self.ref.L.ref_case_write_checkpoint(self.h, path.encode()):
+            raise RuntimeError(self.ref.err())
+
+    def read_checkpoint(self, path: str):
+        """io.hpp:112-145 read_checkpoint (restores state, boundary and body positions)."""
+        if self.ref.L.ref_case_read_checkpoint(self.h, path.encode()):
+            raise RuntimeError(self.ref.err())
 
     def step(self) -> dict:
         rep = np.zeros(len(self.STEP_KEYS))

@@ -368,4 +368,24 @@ int ref_case_visc_bc(const void* h, double* out) {
     return static_cast<int>(v.size());
 }
 
+// io.hpp:89-145 checkpoints (text, %.17g): 0 on success
+int ref_case_write_checkpoint(const void* h, const char* path) {
+    try {
+        write_checkpoint(path, *static_cast<const RefCase*>(h)->st);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+int ref_case_read_checkpoint(void* h, const char* path) {
+    try {
+        read_checkpoint(path, *static_cast<RefCase*>(h)->st);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 }  // extern "C"

@@ -571,6 +571,72 @@ class Stepper:
                                                                     ("x", "y", "ub_x", "ub_y", "ds")]))
         return {k: v[:self.n_b] for k, v in out.items()}
 
+    _CKPT_BOUNDARY = ("left_u", "right_u", "left_v", "right_v", "bottom_v", "top_v", "bottom_u", "top_u")
+
+    def _boundary_sizes(self):
+        nx, ny = self.nx, self.ny
+        return (ny, ny, ny - 1, ny - 1, nx, nx, nx - 1, nx - 1)
+
+    def write_checkpoint(self, path: str):
+        """write_checkpoint (io.hpp:89-110): the reference's 'ibmcfd-checkpoint 1' text format,
+        every double as %.17g (exact round trip), readable by the reference's read_checkpoint."""
+        t, step, have = self.get("scalars")
+
+        def block(f, name, a):
+            f.write(f"{name} {len(a)}\n")
+            if len(a):
+                np.savetxt(f, np.asarray(a, np.float64), fmt="%.17g")
+
+        with open(path, "w") as f:
+            f.write("ibmcfd-checkpoint 1\n")
+            f.write("t %.17g\n" % t)
+            f.write("step %d\n" % int(step))
+            f.write("have_conv %d\n" % (1 if have else 0))
+            block(f, "q", self.get("q"))
+            block(f, "conv_prev", self.get("conv_prev"))
+            block(f, "lambda", self.get("lambda"))
+            bnd = self.get("boundary")
+            o = 0
+            for name, n in zip(self._CKPT_BOUNDARY, self._boundary_sizes()):
+                block(f, name, bnd[o:o + n])
+                o += n
+
+    def read_checkpoint(self, path: str):
+        """read_checkpoint (io.hpp:112-145): restores t, step, have_conv, q, conv_prev, lambda and
+        the boundary arrays; body positions follow the restored time (sync_bodies_to_time)."""
+        with open(path) as f:
+            tok = f.read().split()
+        pos = 0
+
+        def take(n=1):
+            nonlocal pos
+            out = tok[pos:pos + n]
+            pos += n
+            return out
+
+        magic, ver = take(2)
+        if magic != "ibmcfd-checkpoint" or ver != "1":
+            raise RuntimeError(f"checkpoint: bad header in {path}")
+        vals = {}
+        for key in ("t", "step", "have_conv"):
+            k, v = take(2)
+            if k != key:
+                raise RuntimeError(f"checkpoint: missing {key}")
+            vals[key] = float(v)
+        blocks = {}
+        for name in ("q", "conv_prev", "lambda") + self._CKPT_BOUNDARY:
+            k, n = take(2)
+            if k != name:
+                raise RuntimeError(f"checkpoint: expected block '{name}', found '{k}'")
+            blocks[name] = np.array([float(x) for x in take(int(n))], np.float64)
+        if len(blocks["q"]) != self.n_q:
+            raise RuntimeError("checkpoint: grid size mismatch")
+        self.set("q", blocks["q"])
+        self.set("conv_prev", blocks["conv_prev"])
+        self.set("lambda", blocks["lambda"])
+        self.set("boundary", np.concatenate([blocks[n] for n in self._CKPT_BOUNDARY]))
+        self.set("scalars", np.array([vals["t"], vals["step"], vals["have_conv"]]))
+
     def vorticity(self) -> np.ndarray:
         """compute_vorticity (diagnostics.hpp:42-56) of the current q, on the device."""
         n = C.c_int()
