@@ -39,6 +39,13 @@ int main(int argc, char** argv) {
                         rep.solve2_iters, rep.div_residual, rep.noslip_residual, f[2]);
             if (!rep.ok) return 1;
         }
+        // io.hpp checkpoint round trip: a second stepper resumes from the file and stays identical
+        write_checkpoint("/tmp/ibm_b200_drop_in.ckpt", st);
+        Stepper resumed(argv[1]);
+        read_checkpoint("/tmp/ibm_b200_drop_in.ckpt", resumed);
+        const bool same = st.advance().ok && resumed.advance().ok && st.q() == resumed.q();
+        std::printf("checkpoint resume %s\n", same ? "bitwise identical" : "DIFFERS");
+        if (!same) return 1;
     }
     try {
         SolverParams bad;

@@ -6,6 +6,8 @@
 // arguments, std::runtime_error otherwise). Host std::vector in and out, exactly as the
 // reference's value semantics; the device keeps its own copies.
 #pragma once
+#include <cstdio>
+#include <fstream>
 #include <memory>
 #include <type_traits>
 #include <stdexcept>
@@ -358,7 +360,8 @@ public:
         return SparseMatrix::borrowed(m);
     }
 
-private:
+    // raw state access (ibmgpu_stepper_get/set codes: 0 q, 1 lambda, 2 conv_prev, 3 boundary,
+    // 4 {t, step, have_conv}, 5 f~) — what write_checkpoint / read_checkpoint below use
     std::vector<double> get(int which) const {
         int n = 0;
         check(ibmgpu_stepper_get(h_.get(), which, nullptr, &n));
@@ -366,10 +369,85 @@ private:
         check(ibmgpu_stepper_get(h_.get(), which, v.data(), &n));
         return v;
     }
+    void set(int which, const std::vector<double>& v) {
+        check(ibmgpu_stepper_set(h_.get(), which, v.data(), static_cast<int>(v.size())));
+    }
+    std::pair<int, int> grid_dims() const {
+        int d[8];
+        check(ibmgpu_stepper_dims(h_.get(), d));
+        return {d[0], d[1]};
+    }
+
+private:
     struct Del {
         void operator()(ibmgpu_stepper_t s) const { ibmgpu_stepper_destroy(s); }
     };
     std::unique_ptr<ibmgpu_stepper, Del> h_;
 };
+
+// io.hpp:89-110 write_checkpoint: "ibmcfd-checkpoint 1", every double as %.17g
+inline void write_checkpoint(const std::string& path, const Stepper& st) {
+    std::FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) throw std::runtime_error("cannot open " + path);
+    const auto sc = st.get(4);
+    auto block = [&](const char* name, const double* v, size_t n) {
+        std::fprintf(f, "%s %zu\n", name, n);
+        for (size_t i = 0; i < n; ++i) std::fprintf(f, "%.17g\n", v[i]);
+    };
+    std::fprintf(f, "ibmcfd-checkpoint 1\n");
+    std::fprintf(f, "t %.17g\n", sc[0]);
+    std::fprintf(f, "step %d\n", static_cast<int>(sc[1]));
+    std::fprintf(f, "have_conv %d\n", sc[2] != 0.0 ? 1 : 0);
+    const auto q = st.get(0), cp = st.get(2), lam = st.get(1), bnd = st.get(3);
+    block("q", q.data(), q.size());
+    block("conv_prev", cp.data(), cp.size());
+    block("lambda", lam.data(), lam.size());
+    const auto [nx, ny] = st.grid_dims();
+    const char* names[8] = {"left_u", "right_u", "left_v", "right_v", "bottom_v", "top_v", "bottom_u", "top_u"};
+    const size_t sizes[8] = {size_t(ny), size_t(ny), size_t(ny - 1), size_t(ny - 1),
+                             size_t(nx), size_t(nx), size_t(nx - 1), size_t(nx - 1)};
+    size_t o = 0;
+    for (int k = 0; k < 8; ++k) {
+        block(names[k], bnd.data() + o, sizes[k]);
+        o += sizes[k];
+    }
+    std::fclose(f);
+}
+
+// io.hpp:112-145 read_checkpoint (bodies follow the restored time, as sync_bodies_to_time)
+inline void read_checkpoint(const std::string& path, Stepper& st) {
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("cannot open " + path);
+    std::string magic, key;
+    int version = 0;
+    if (!(in >> magic >> version) || magic != "ibmcfd-checkpoint" || version != 1)
+        throw std::runtime_error("checkpoint: bad header in " + path);
+    double t = 0;
+    int step = 0, have = 0;
+    if (!(in >> key >> t) || key != "t") throw std::runtime_error("checkpoint: missing t");
+    if (!(in >> key >> step) || key != "step") throw std::runtime_error("checkpoint: missing step");
+    if (!(in >> key >> have) || key != "have_conv") throw std::runtime_error("checkpoint: missing have_conv");
+    auto block = [&](const std::string& expect) {
+        std::string name;
+        size_t n = 0;
+        if (!(in >> name >> n) || name != expect)
+            throw std::runtime_error("checkpoint: expected block '" + expect + "', found '" + name + "'");
+        std::vector<double> v(n);
+        for (auto& x : v)
+            if (!(in >> x)) throw std::runtime_error("checkpoint: truncated block " + expect);
+        return v;
+    };
+    const auto q = block("q"), cp = block("conv_prev"), lam = block("lambda");
+    std::vector<double> bnd;
+    for (const char* n : {"left_u", "right_u", "left_v", "right_v", "bottom_v", "top_v", "bottom_u", "top_u"}) {
+        const auto b = block(n);
+        bnd.insert(bnd.end(), b.begin(), b.end());
+    }
+    st.set(0, q);
+    st.set(2, cp);
+    st.set(1, lam);
+    st.set(3, bnd);
+    st.set(4, {t, double(step), double(have)});
+}
 
 }  // namespace ibm_b200

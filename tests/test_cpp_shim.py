@@ -31,3 +31,4 @@ def test_cpp_shim_runs_reference_sequence():
     assert r.returncode == 0, r.stdout + r.stderr
     assert "converged" in r.stdout and "invalid_argument" in r.stdout
     assert r.stdout.count("ok=1") == 3
+    assert "checkpoint resume bitwise identical" in r.stdout
