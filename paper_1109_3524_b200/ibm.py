@@ -811,3 +811,102 @@ class DistSolver:
             self.ctx.lib.ibmgpu_dist_destroy(self.h)
         except Exception:
             pass
+
+
+# ----------------------------------------------------------------------------- run loop (runner.hpp)
+def _cfg_values(cfg_path: str) -> dict:
+    """The run-loop keys of a case file ([time] n_steps/n_out, [output] dir/checkpoint_every);
+    everything else is parsed by the native case loader."""
+    vals, sec = {}, ""
+    with open(cfg_path) as f:
+        for raw in f:
+            line = raw.split("#", 1)[0].strip()
+            if not line:
+                continue
+            if line.startswith("["):
+                sec = line.strip("[]").strip()
+                continue
+            if "=" in line:
+                k, v = (x.strip() for x in line.split("=", 1))
+                vals[f"{sec}.{k}"] = v
+    return vals
+
+
+@dataclass
+class RunResult:
+    """runner.hpp:44-55 RunResult (the fields a caller reads)."""
+    exit_code: int = 0
+    message: str = ""
+    steps_done: int = 0
+    total_solve1_iters: int = 0
+    total_solve2_iters: int = 0
+    hierarchy_builds: int = 1
+    max_div_residual: float = 0.0
+    max_noslip_residual: float = 0.0
+    force_t: list = field(default_factory=list)
+    force_cd: list = field(default_factory=list)
+    force_cl: list = field(default_factory=list)
+
+
+def run_case(cfg_path: str, out_dir: str | None = None, n_steps: int = 0, resume_from: str = "",
+             quiet: bool = True, **stepper_kw) -> RunResult:
+    """run_case (runner.hpp:77-164) on the device stepper, with the reference's output files:
+    forces.csv ("t,fx,fy,cd,cl", %.17g), vorticity_<k>.txt every n_out steps and at the end
+    ("x y omega", %.9g), checkpoint_<k>.txt every checkpoint_every steps and checkpoint_final.txt
+    (io.hpp format)."""
+    import os
+    v = _cfg_values(cfg_path)
+    out = out_dir or v.get("output.dir", "out")
+    os.makedirs(out, exist_ok=True)
+    n_total = n_steps or int(v.get("time.n_steps", "0"))
+    n_out = int(v.get("time.n_out", "0"))
+    ckpt_every = int(v.get("output.checkpoint_every", "0"))
+    st = Stepper(cfg_path, **stepper_kw)
+    if resume_from:
+        st.read_checkpoint(resume_from)
+    g = st.grid()
+    res = RunResult()
+    start = int(st.get("scalars")[1])
+    last_ckpt = ""
+
+    def vort(path):
+        w = st.vorticity()
+        xs, ys = g["x_faces"][1:st.nx], g["y_faces"][1:st.ny]
+        X, Y = np.meshgrid(xs, ys)
+        with open(path, "w") as f:
+            f.write(f"# vorticity at interior vertices: x y omega ({st.nx - 1} x {st.ny - 1})\n")
+            np.savetxt(f, np.column_stack([X.ravel(), Y.ravel(), w]), fmt="%.9g")
+
+    with open(os.path.join(out, "forces.csv"), "w") as fw:
+        fw.write("t,fx,fy,cd,cl\n")
+        for k in range(start, n_total):
+            rep = st.advance()
+            res.total_solve1_iters += rep.solve1_iters
+            res.total_solve2_iters += rep.solve2_iters
+            res.hierarchy_builds += int(rep.rebuilt_hierarchy)
+            res.max_div_residual = max(res.max_div_residual, rep.div_residual)
+            res.max_noslip_residual = max(res.max_noslip_residual, rep.noslip_residual)
+            if not rep.ok:
+                res.exit_code = 1
+                res.message = rep.message + (f"; last good checkpoint: {last_ckpt}" if last_ckpt else "")
+                return res
+            if st.n_b > 0:
+                f = st.forces()
+                t = float(st.get("scalars")[0])
+                fw.write("%.17g,%.17g,%.17g,%.17g,%.17g\n" % (t, f["fx"], f["fy"], f["cd"], f["cl"]))
+                fw.flush()
+                res.force_t.append(t)
+                res.force_cd.append(f["cd"])
+                res.force_cl.append(f["cl"])
+            if n_out > 0 and (k + 1) % n_out == 0:
+                vort(os.path.join(out, f"vorticity_{k + 1}.txt"))
+            if ckpt_every > 0 and (k + 1) % ckpt_every == 0:
+                last_ckpt = os.path.join(out, f"checkpoint_{k + 1}.txt")
+                st.write_checkpoint(last_ckpt)
+            res.steps_done = k + 1
+            if not quiet and ((k + 1) % 100 == 0 or k + 1 == n_total):
+                print(f"step {k + 1:6d}/{n_total}  s1 {rep.solve1_iters:3d}  s2 {rep.solve2_iters:3d}  "
+                      f"div {rep.div_residual:.2e}  slip {rep.noslip_residual:.2e}")
+    vort(os.path.join(out, "vorticity_final.txt"))
+    st.write_checkpoint(os.path.join(out, "checkpoint_final.txt"))
+    return res

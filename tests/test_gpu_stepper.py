@@ -175,3 +175,27 @@ def test_checkpoint_format_interoperates_with_reference(ref, tmp_path, name):
         assert np.array_equal(again.get("q"), st.get("q")) and np.array_equal(again.get("lambda"), st.get("lambda"))
     else:
         assert H.rel_err(again.get("q"), st.get("q")) <= 1e-9
+
+
+def test_run_case_outputs_match_reference_and_are_deterministic(ref, tmp_path):
+    """run_case (runner.hpp:77-164): forces.csv rows follow the reference's per-step forces, two runs
+    write byte-identical forces.csv (test_config.cpp:288-305), and the final checkpoint resumes."""
+    name = "cylinder_re40_smoke"
+    r1 = ibm.run_case(H.case(name), out_dir=str(tmp_path / "a"), n_steps=4)
+    r2 = ibm.run_case(H.case(name), out_dir=str(tmp_path / "b"), n_steps=4)
+    assert r1.exit_code == 0 and r1.steps_done == 4
+    a = (tmp_path / "a" / "forces.csv").read_bytes()
+    assert a == (tmp_path / "b" / "forces.csv").read_bytes()
+    rows = a.decode().splitlines()
+    assert rows[0] == "t,fx,fy,cd,cl" and len(rows) == 5
+    rc = ref.case(H.case(name))
+    for row in rows[1:]:
+        rc.step()
+        t, fx, fy, cd, cl = map(float, row.split(","))
+        fr = rc.forces()
+        assert abs(cd - fr["cd"]) <= 1e-6 * abs(fr["cd"]) and abs(t - rc.time()) <= 1e-12
+    vort = (tmp_path / "a" / "vorticity_final.txt").read_text().splitlines()
+    assert vort[0].startswith("# vorticity at interior vertices")
+    r3 = ibm.run_case(H.case(name), out_dir=str(tmp_path / "c"), n_steps=6,
+                      resume_from=str(tmp_path / "a" / "checkpoint_final.txt"))
+    assert r3.exit_code == 0 and r3.steps_done == 6
