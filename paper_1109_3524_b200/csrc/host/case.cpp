@@ -2,6 +2,8 @@
 // association order (built with -ffp-contract=off) so every coordinate is bit-identical.
 #include "case.hpp"
 
+#include <omp.h>
+
 #include <algorithm>
 #include <cmath>
 #include <fstream>
@@ -575,139 +577,199 @@ Case parse_case(const std::string& path) {
 // ---------------------------------------------------------------- grid operators
 std::vector<double> metric(const Grid& g) {
     std::vector<double> m(g.n_q());
+#pragma omp parallel for schedule(static)
     for (int j = 0; j < g.ny; ++j)
         for (int i_f = 1; i_f < g.nx; ++i_f) m[g.u_id(i_f, j)] = g.del_x[i_f - 1] / g.dy[j];
+#pragma omp parallel for schedule(static)
     for (int j_f = 1; j_f < g.ny; ++j_f)
         for (int i = 0; i < g.nx; ++i) m[g.v_id(i, j_f)] = g.del_y[j_f - 1] / g.dx[i];
     return m;
 }
 
-// Flux-form staggered Laplacian on q (operators.hpp:94-194), emitted directly in CSR column
-// order (south, west, diagonal, east, north); wall neighbours become BcCouplings in the
-// reference's per-row order (u: W, E, S, N; v: S, N, W, E).
+namespace {
+// One row of the flux-form staggered Laplacian (operators.hpp:94-194): candidates in CSR column
+// order (south, west, diagonal, east, north) and the wall couplings in the reference's per-row
+// order (u: W, E, S, N; v: S, N, W, E). Exact zeros are dropped as from_triplets does.
+struct LRow {
+    int n = 0, nb = 0;
+    int c[5];
+    double v[5];
+    BcCoupling b[4];
+    void put(int col, double val) {
+        if (val != 0.0) c[n] = col, v[n] = val, ++n;  // from_triplets drops exact zeros (sparse.hpp:59)
+    }
+};
+
+void u_row(const Grid& g, int j, int i_f, LRow& o) {
+    const int nx = g.nx, ny = g.ny;
+    const int row = g.u_id(i_f, j);
+    const double sm = g.del_x[i_f - 1], dyj = g.dy[j];
+    double dh = 0.0;
+    double wv = 0, ev = 0, sv = 0, nv = 0;
+    const bool hw = i_f - 1 >= 1, he = i_f + 1 <= nx - 1, hs = j > 0, hn = j < ny - 1;
+    {
+        const double w_hat = 1.0 / (sm * g.dx[i_f - 1]);
+        dh += w_hat;
+        if (hw) wv = 1.0 / (dyj * g.dx[i_f - 1]);
+        else o.b[o.nb++] = {row, LU, j, sm * w_hat};
+    }
+    {
+        const double w_hat = 1.0 / (sm * g.dx[i_f]);
+        dh += w_hat;
+        if (he) ev = 1.0 / (dyj * g.dx[i_f]);
+        else o.b[o.nb++] = {row, RU, j, sm * w_hat};
+    }
+    {
+        const double span = hs ? g.del_y[j - 1] : 0.5 * dyj;
+        const double w_hat = 1.0 / (dyj * span);
+        dh += w_hat;
+        if (hs) sv = sm / (span * (dyj * g.dy[j - 1]));
+        else o.b[o.nb++] = {row, BU, i_f - 1, sm * w_hat};
+    }
+    {
+        const double span = hn ? g.del_y[j] : 0.5 * dyj;
+        const double w_hat = 1.0 / (dyj * span);
+        dh += w_hat;
+        if (hn) nv = sm / (span * (dyj * g.dy[j + 1]));
+        else o.b[o.nb++] = {row, TU, i_f - 1, sm * w_hat};
+    }
+    if (hs) o.put(g.u_id(i_f, j - 1), sv);
+    if (hw) o.put(g.u_id(i_f - 1, j), wv);
+    o.put(row, -sm * dh / dyj);
+    if (he) o.put(g.u_id(i_f + 1, j), ev);
+    if (hn) o.put(g.u_id(i_f, j + 1), nv);
+}
+
+void v_row(const Grid& g, int j_f, int i, LRow& o) {
+    const int nx = g.nx, ny = g.ny;
+    const int row = g.v_id(i, j_f);
+    const double sm = g.del_y[j_f - 1], dxi = g.dx[i];
+    double dh = 0.0;
+    double wv = 0, ev = 0, sv = 0, nv = 0;
+    const bool hs = j_f - 1 >= 1, hn = j_f + 1 <= ny - 1, hw = i > 0, he = i < nx - 1;
+    {
+        const double w_hat = 1.0 / (sm * g.dy[j_f - 1]);
+        dh += w_hat;
+        if (hs) sv = 1.0 / (dxi * g.dy[j_f - 1]);
+        else o.b[o.nb++] = {row, BV, i, sm * w_hat};
+    }
+    {
+        const double w_hat = 1.0 / (sm * g.dy[j_f]);
+        dh += w_hat;
+        if (hn) nv = 1.0 / (dxi * g.dy[j_f]);
+        else o.b[o.nb++] = {row, TV, i, sm * w_hat};
+    }
+    {
+        const double span = hw ? g.del_x[i - 1] : 0.5 * dxi;
+        const double w_hat = 1.0 / (dxi * span);
+        dh += w_hat;
+        if (hw) wv = sm / (span * (dxi * g.dx[i - 1]));
+        else o.b[o.nb++] = {row, LV, j_f - 1, sm * w_hat};
+    }
+    {
+        const double span = he ? g.del_x[i] : 0.5 * dxi;
+        const double w_hat = 1.0 / (dxi * span);
+        dh += w_hat;
+        if (he) ev = sm / (span * (dxi * g.dx[i + 1]));
+        else o.b[o.nb++] = {row, RV, j_f - 1, sm * w_hat};
+    }
+    if (hs) o.put(g.v_id(i, j_f - 1), sv);
+    if (hw) o.put(g.v_id(i - 1, j_f), wv);
+    o.put(row, -sm * dh / dxi);
+    if (he) o.put(g.v_id(i + 1, j_f), ev);
+    if (hn) o.put(g.v_id(i, j_f + 1), nv);
+}
+}  // namespace
+
+// Emitted directly in CSR, in parallel over grid rows: pass 1 counts each row's entries, pass 2
+// recomputes the same row (identical arithmetic) and writes it at its offset. BcCouplings are
+// gathered per thread over contiguous row ranges and concatenated in row order.
 Csr diffusion(const Grid& g, std::vector<BcCoupling>& bc) {
     bc.clear();
     const int nx = g.nx, ny = g.ny;
     Csr L;
     L.rows = L.cols = g.n_q();
-    L.rp.reserve(L.rows + 1);
-    L.ci.reserve(static_cast<size_t>(L.rows) * 5);
-    L.v.reserve(static_cast<size_t>(L.rows) * 5);
-    L.rp.push_back(0);
-    auto emit = [&](int row, bool has_s, int s_col, double s_val, bool has_w, int w_col, double w_val, double d,
-                    bool has_e, int e_col, double e_val, bool has_n, int n_col, double n_val) {
-        auto put = [&](int c, double v) {
-            if (v != 0.0) {  // from_triplets drops exact zeros (sparse.hpp:59)
-                L.ci.push_back(c);
-                L.v.push_back(v);
-            }
-        };
-        if (has_s) put(s_col, s_val);
-        if (has_w) put(w_col, w_val);
-        put(row, d);
-        if (has_e) put(e_col, e_val);
-        if (has_n) put(n_col, n_val);
-        L.rp.push_back(static_cast<int>(L.ci.size()));
-    };
+    std::vector<int, UninitAlloc<int>> cnt(static_cast<size_t>(L.rows));
+#pragma omp parallel for schedule(static)
     for (int j = 0; j < ny; ++j)
         for (int i_f = 1; i_f < nx; ++i_f) {
-            const int row = g.u_id(i_f, j);
-            const double sm = g.del_x[i_f - 1], dyj = g.dy[j];
-            double dh = 0.0;
-            double wv = 0, ev = 0, sv = 0, nv = 0;
-            const bool hw = i_f - 1 >= 1, he = i_f + 1 <= nx - 1, hs = j > 0, hn = j < ny - 1;
-            {
-                const double w_hat = 1.0 / (sm * g.dx[i_f - 1]);
-                dh += w_hat;
-                if (hw) wv = 1.0 / (dyj * g.dx[i_f - 1]);
-                else bc.push_back({row, LU, j, sm * w_hat});
-            }
-            {
-                const double w_hat = 1.0 / (sm * g.dx[i_f]);
-                dh += w_hat;
-                if (he) ev = 1.0 / (dyj * g.dx[i_f]);
-                else bc.push_back({row, RU, j, sm * w_hat});
-            }
-            {
-                const double span = hs ? g.del_y[j - 1] : 0.5 * dyj;
-                const double w_hat = 1.0 / (dyj * span);
-                dh += w_hat;
-                if (hs) sv = sm / (span * (dyj * g.dy[j - 1]));
-                else bc.push_back({row, BU, i_f - 1, sm * w_hat});
-            }
-            {
-                const double span = hn ? g.del_y[j] : 0.5 * dyj;
-                const double w_hat = 1.0 / (dyj * span);
-                dh += w_hat;
-                if (hn) nv = sm / (span * (dyj * g.dy[j + 1]));
-                else bc.push_back({row, TU, i_f - 1, sm * w_hat});
-            }
-            emit(row, hs, g.u_id(i_f, j - 1), sv, hw, g.u_id(i_f - 1, j), wv, -sm * dh / dyj, he, g.u_id(i_f + 1, j),
-                 ev, hn, g.u_id(i_f, j + 1), nv);
+            LRow o;
+            u_row(g, j, i_f, o);
+            cnt[g.u_id(i_f, j)] = o.n;
         }
+#pragma omp parallel for schedule(static)
     for (int j_f = 1; j_f < ny; ++j_f)
         for (int i = 0; i < nx; ++i) {
-            const int row = g.v_id(i, j_f);
-            const double sm = g.del_y[j_f - 1], dxi = g.dx[i];
-            double dh = 0.0;
-            double wv = 0, ev = 0, sv = 0, nv = 0;
-            const bool hs = j_f - 1 >= 1, hn = j_f + 1 <= ny - 1, hw = i > 0, he = i < nx - 1;
-            {
-                const double w_hat = 1.0 / (sm * g.dy[j_f - 1]);
-                dh += w_hat;
-                if (hs) sv = 1.0 / (dxi * g.dy[j_f - 1]);
-                else bc.push_back({row, BV, i, sm * w_hat});
-            }
-            {
-                const double w_hat = 1.0 / (sm * g.dy[j_f]);
-                dh += w_hat;
-                if (hn) nv = 1.0 / (dxi * g.dy[j_f]);
-                else bc.push_back({row, TV, i, sm * w_hat});
-            }
-            {
-                const double span = hw ? g.del_x[i - 1] : 0.5 * dxi;
-                const double w_hat = 1.0 / (dxi * span);
-                dh += w_hat;
-                if (hw) wv = sm / (span * (dxi * g.dx[i - 1]));
-                else bc.push_back({row, LV, j_f - 1, sm * w_hat});
-            }
-            {
-                const double span = he ? g.del_x[i] : 0.5 * dxi;
-                const double w_hat = 1.0 / (dxi * span);
-                dh += w_hat;
-                if (he) ev = sm / (span * (dxi * g.dx[i + 1]));
-                else bc.push_back({row, RV, j_f - 1, sm * w_hat});
-            }
-            emit(row, hs, g.v_id(i, j_f - 1), sv, hw, g.v_id(i - 1, j_f), wv, -sm * dh / dxi, he, g.v_id(i + 1, j_f),
-                 ev, hn, g.v_id(i, j_f + 1), nv);
+            LRow o;
+            v_row(g, j_f, i, o);
+            cnt[g.v_id(i, j_f)] = o.n;
         }
+    L.rp.resize(static_cast<size_t>(L.rows) + 1);
+    L.rp[0] = 0;
+    for (int r = 0; r < L.rows; ++r) L.rp[r + 1] = L.rp[r] + cnt[r];
+    L.ci.resize(static_cast<size_t>(L.rp[L.rows]));
+    L.v.resize(L.ci.size());
+    auto fill = [&](const LRow& o, int row) {
+        const int p = L.rp[row];
+        for (int k = 0; k < o.n; ++k) L.ci[p + k] = o.c[k], L.v[p + k] = o.v[k];
+    };
+    int nt = 1;
+#pragma omp parallel
+#pragma omp single
+    nt = omp_get_num_threads();
+    std::vector<std::vector<BcCoupling>> tb(static_cast<size_t>(nt));
+#pragma omp parallel num_threads(nt)
+    {
+        auto& mine = tb[static_cast<size_t>(omp_get_thread_num())];
+#pragma omp for schedule(static)
+        for (int j = 0; j < ny; ++j)
+            for (int i_f = 1; i_f < nx; ++i_f) {
+                LRow o;
+                u_row(g, j, i_f, o);
+                fill(o, g.u_id(i_f, j));
+                for (int k = 0; k < o.nb; ++k) mine.push_back(o.b[k]);
+            }
+    }
+    for (auto& t : tb) bc.insert(bc.end(), t.begin(), t.end()), t.clear();
+#pragma omp parallel num_threads(nt)
+    {
+        auto& mine = tb[static_cast<size_t>(omp_get_thread_num())];
+#pragma omp for schedule(static)
+        for (int j_f = 1; j_f < ny; ++j_f)
+            for (int i = 0; i < nx; ++i) {
+                LRow o;
+                v_row(g, j_f, i, o);
+                fill(o, g.v_id(i, j_f));
+                for (int k = 0; k < o.nb; ++k) mine.push_back(o.b[k]);
+            }
+    }
+    for (auto& t : tb) bc.insert(bc.end(), t.begin(), t.end());
     return L;
 }
 
-// operators.hpp:210-226 (entries +-1; D = -G^T)
+// operators.hpp:210-226 (entries +-1; D = -G^T): two entries per row, written in parallel
 Csr gradient(const Grid& g) {
     Csr G;
     G.rows = g.n_q();
     G.cols = g.n_p();
-    G.rp.reserve(G.rows + 1);
-    G.ci.reserve(static_cast<size_t>(G.rows) * 2);
-    G.v.reserve(static_cast<size_t>(G.rows) * 2);
-    G.rp.push_back(0);
+    G.rp.resize(static_cast<size_t>(G.rows) + 1);
+    G.ci.resize(static_cast<size_t>(G.rows) * 2);
+    G.v.resize(static_cast<size_t>(G.rows) * 2);
+#pragma omp parallel for schedule(static)
+    for (long long r = 0; r <= G.rows; ++r) G.rp[r] = static_cast<int>(2 * r);
+#pragma omp parallel for schedule(static)
     for (int j = 0; j < g.ny; ++j)
         for (int i_f = 1; i_f < g.nx; ++i_f) {
-            G.ci.push_back(g.p_id(i_f - 1, j));
-            G.v.push_back(-1.0);
-            G.ci.push_back(g.p_id(i_f, j));
-            G.v.push_back(1.0);
-            G.rp.push_back(static_cast<int>(G.ci.size()));
+            const size_t p = 2 * static_cast<size_t>(g.u_id(i_f, j));
+            G.ci[p] = g.p_id(i_f - 1, j), G.v[p] = -1.0;
+            G.ci[p + 1] = g.p_id(i_f, j), G.v[p + 1] = 1.0;
         }
+#pragma omp parallel for schedule(static)
     for (int j_f = 1; j_f < g.ny; ++j_f)
         for (int i = 0; i < g.nx; ++i) {
-            G.ci.push_back(g.p_id(i, j_f - 1));
-            G.v.push_back(-1.0);
-            G.ci.push_back(g.p_id(i, j_f));
-            G.v.push_back(1.0);
-            G.rp.push_back(static_cast<int>(G.ci.size()));
+            const size_t p = 2 * static_cast<size_t>(g.v_id(i, j_f));
+            G.ci[p] = g.p_id(i, j_f - 1), G.v[p] = -1.0;
+            G.ci[p + 1] = g.p_id(i, j_f), G.v[p + 1] = 1.0;
         }
     return G;
 }

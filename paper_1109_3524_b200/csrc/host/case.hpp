@@ -8,6 +8,8 @@
 #pragma once
 #include <limits>
 #include <string>
+#include <memory>
+#include <utility>
 #include <vector>
 
 namespace ibmhost {
@@ -117,10 +119,29 @@ Case parse_case(const std::string& path);
 std::vector<Body> build_bodies(const Case& c);
 
 // ---- grid operators (host CSR) ----
+// Default-initialising allocator: resize() leaves the storage untouched, so the parallel fill
+// below is the first touch (a 64M-cell L is 8 GB; zeroing it first on one thread doubled setup).
+template <class T>
+struct UninitAlloc : std::allocator<T> {
+    using std::allocator<T>::allocator;
+    template <class U>
+    struct rebind {
+        using other = UninitAlloc<U>;
+    };
+    template <class U>
+    void construct(U* p) noexcept {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <class U, class... Args>
+    void construct(U* p, Args&&... args) {
+        ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+    }
+};
+
 struct Csr {
     int rows = 0, cols = 0;
-    std::vector<int> rp, ci;
-    std::vector<double> v;
+    std::vector<int, UninitAlloc<int>> rp, ci;
+    std::vector<double, UninitAlloc<double>> v;
 };
 
 enum Slot { LU, RU, LV, RV, BV, TV, BU, TU };

@@ -18,6 +18,7 @@
 // This file is compiled with --fmad=false: every expression rounds like the reference's.
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -376,6 +377,24 @@ double host_from_bits(unsigned long long b) {
 }  // namespace
 
 namespace {
+// operators.hpp:350-374 diagonal terms: M/dt, 1/M, dt * (1/M)
+__global__ void k_metric_terms(long long n, const double* __restrict__ M, double dt, double* __restrict__ mdt,
+                               double* __restrict__ minv, double* __restrict__ d) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double m = M[i];
+    mdt[i] = __ddiv_rn(m, dt);
+    const double mi = __ddiv_rn(1.0, m);
+    minv[i] = mi;
+    d[i] = __dmul_rn(dt, mi);
+}
+__global__ void k_fill(long long n, double v, double* __restrict__ out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = v;
+}
+}  // namespace
+
+namespace {
 // compute_vorticity (diagnostics.hpp:42-56): omega = dv/dx - du/dy at the interior vertices,
 // row-major in j, same operation order (bit-exact)
 __global__ void k_vorticity(int nx, int ny, const double* __restrict__ dx, const double* __restrict__ dy,
@@ -579,6 +598,16 @@ namespace {
 
 void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides* ov) {
     Ctx* c = S->c;
+    // IBMGPU_SETUP_PROFILE=1: wall time of each setup phase on stderr
+    const bool prof = std::getenv("IBMGPU_SETUP_PROFILE") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!prof) return;
+        sync(c);
+        const auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[setup] %-22s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    };
     S->cfg = ibmhost::parse_case(path);
     auto& cfg = S->cfg;
     if (ov) {
@@ -614,6 +643,7 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
     const std::vector<double> M = ibmhost::metric(g);
     const ibmhost::Csr Lh = ibmhost::diffusion(g, vbc);
     const ibmhost::Csr Gh = ibmhost::gradient(g);
+    lap("host M, L, G");
     S->L = mat_upload(c, Lh.rows, Lh.cols, (int)Lh.ci.size(), Lh.rp.data(), Lh.ci.data(), Lh.v.data());
     S->G = mat_upload(c, Gh.rows, Gh.cols, (int)Gh.ci.size(), Gh.rp.data(), Gh.ci.data(), Gh.v.data());
 
@@ -626,38 +656,34 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
     up(S->dy, g.dy);
     up(S->del_x, g.del_x);
     up(S->del_y, g.del_y);
+    lap("upload L, G, grid");
 
-    // A = M/dt - (nu/2) L ; B^N (operators.hpp:350-374) on the device
+    // A = M/dt - (nu/2) L ; B^N (operators.hpp:350-374) on the device; M/dt, 1/M and dt/M are
+    // formed from M on the device with the reference's rounding (one IEEE op each)
     const size_t nq = (size_t)S->n_q;
-    std::vector<double> m_dt(nq), minv(nq), d(nq);
-    for (size_t i = 0; i < nq; ++i) {
-        m_dt[i] = M[i] / S->dt;
-        minv[i] = 1.0 / M[i];
-        d[i] = S->dt * minv[i];
-    }
-    up(S->mdt, m_dt);
+    require(S->dt > 0.0, "operators: dt must be positive");
+    require(S->n_order >= 1 && S->n_order <= 3, "operators: B^N order must be 1, 2 or 3");
+    DBuf<double> dd(c, nq), mi(c, nq);
     {
-        DBuf<double> md(c, nq);
-        h2d(c, md.p, m_dt.data(), nq);
-        Mat* Dm = diag_matrix(c, S->n_q, md.p);
+        DBuf<double> Md(c, nq);
+        h2d(c, Md.p, M.data(), nq);
+        S->mdt.alloc(c, nq);
+        k_metric_terms<<<blocks((long long)nq), 256, 0, c->stream>>>((long long)nq, Md.p, S->dt, S->mdt.p, mi.p, dd.p);
+        CK_LAUNCH(c);
+        Mat* Dm = diag_matrix(c, S->n_q, S->mdt.p);
         S->A = add(c, 1.0, Dm, -0.5 * S->nu, S->L);
         delete Dm;
     }
-    require(S->dt > 0.0, "operators: dt must be positive");
-    require(S->n_order >= 1 && S->n_order <= 3, "operators: B^N order must be 1, 2 or 3");
     {
-        DBuf<double> dd(c, nq), mi(c, nq);
-        h2d(c, dd.p, d.data(), nq);
-        h2d(c, mi.p, minv.data(), nq);
         if (S->n_order == 1) {
             S->BN = diag_matrix(c, S->n_q, dd.p);
         } else {
             Mat* Xc = scale(c, S->L, 2, 0.0, mi.p);
             Mat* X = scale(c, Xc, 0, 0.5 * S->nu * S->dt, nullptr);
             delete Xc;
-            std::vector<double> ones(nq, 1.0);
             DBuf<double> on(c, nq);
-            h2d(c, on.p, ones.data(), nq);
+            k_fill<<<blocks((long long)nq), 256, 0, c->stream>>>((long long)nq, 1.0, on.p);
+            CK_LAUNCH(c);
             Mat* I = diag_matrix(c, S->n_q, on.p);
             Mat* series = add(c, 1.0, I, 1.0, X);
             delete I;
@@ -676,6 +702,7 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
     S->bn_diagonal = S->n_order == 1 && S->BN->nnz == S->n_q;
     S->bn_diag.alloc(c, nq);
     diag_of(c, S->BN, S->bn_diag.p);
+    lap("A, B^N");
 
     // body operators + coupled system
     S->px.alloc(c, (size_t)std::max(S->n_b, 1));
@@ -688,12 +715,15 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
                              {g.uniform_region.x0, g.uniform_region.x1, g.uniform_region.y0, g.uniform_region.y1}};
     S->gd = grid_dev_new(c, gdsc);
     S->refresh_body_operators();
+    lap("E, H, Q, Q^T, lhs2");
     for (Mat* m : {S->L, S->A, S->BN, S->G}) mat_plan(c, m);
+    lap("SpMV plans");
 
     // SA hierarchy with the force rows carried to the coarse level (stepper.hpp:179-181)
     S->sa.keep_fine_tail = 2 * S->n_b;
     S->rebuild_hierarchy();
     S->hier->built_at_step = 0;
+    lap("SA hierarchy");
 
     // boundary + state
     S->bl.init(g.nx, g.ny);
