@@ -244,12 +244,15 @@ int ibmgpu_hostcase_free(ibmgpu_hostcase_t h);
  * keeps its owned rows with halo-extended columns, fine levels distributed, levels below
  * min_dist_rows replicated. Context with nranks > 1: NCCL between processes (ibmgpu_init with the
  * id from ibmgpu_nccl_unique_id on rank 0). Single-rank context: virtual_ranks > 1 emulates the
- * whole partition on this GPU (loopback halos), for parity tests of the decomposition. */
+ * whole partition on this GPU (loopback halos), for parity tests of the decomposition; if that
+ * single-rank context also has an NCCL communicator (nccl id given), the loopback halos travel as
+ * ncclSend/ncclRecv pairs to self, so the NCCL p2p path runs on one GPU. */
 typedef struct ibmgpu_dist* ibmgpu_dist_t;
 int ibmgpu_nccl_unique_id(void* id128);
 int ibmgpu_dist_create(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, int precond, ibmgpu_hier_t hier, const int* owner_host,
                        int virtual_ranks, int min_dist_rows, ibmgpu_dist_t* out);
-/* info: nranks, distributed levels, loopback, own rows (first local rank), its A halo, local ranks,
+/* info: nranks, distributed levels, loopback (0 NCCL, 1 device copies, 2 NCCL p2p to self),
+ * own rows (first local rank), its A halo, local ranks,
  * hierarchy levels, SpMV kind of the local A */
 int ibmgpu_dist_info(ibmgpu_dist_t d, int* info8);
 /* b_dev, x_dev: full-length device vectors on every rank; x holds x0 on entry (owned rows used) and

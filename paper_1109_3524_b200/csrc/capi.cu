@@ -360,7 +360,7 @@ int ibmgpu_dist_create(ibmgpu_ctx_t c, ibmgpu_mat_t A, int precond, ibmgpu_hier_
                        int virtual_ranks, int min_dist_rows, ibmgpu_dist_t* out) {
     return guard(c, [&] {
         need(A && owner && out, "dist_create: null argument");
-        need(!c->nccl || virtual_ranks <= 1, "dist_create: virtual ranks need a context without NCCL");
+        need(!c->nccl || c->nranks == 1 || virtual_ranks <= 1, "dist_create: virtual ranks need a single-rank context");
         *out = dist_create(c, A, precond, hier, owner, virtual_ranks, min_dist_rows);
     });
 }

@@ -386,6 +386,7 @@ struct ibmgpu_dist {
     int kind = 0;
     int R = 1;           // ranks of the partition
     bool loop = false;   // loopback (all ranks local)
+    bool loop_nccl = false;  // loopback whose halos travel as NCCL send/recv to self (1-rank comm)
     int D = 0;           // distributed levels
     int n = 0;
     std::vector<std::unique_ptr<ibmgpu::RankData>> ranks;  // local ranks
@@ -426,6 +427,28 @@ void exchange(Dist* d, GetM gm, GetV gv) {
         // copies to separate their cost from the ranks' own work
         static const bool nocopy = std::getenv("IBMGPU_DIST_NOCOPY") != nullptr;
         if (nocopy) return;
+        if (d->loop_nccl) {
+            // every virtual rank's halo through the NCCL p2p path: send/recv pairs to self, issued
+            // in the same order so the k-th send matches the k-th receive
+            const auto& N = nccl_api();
+            auto comm = static_cast<ncclComm_t>(c->nccl);
+            NK(N.groupStart());
+            for (int r = 0; r < d->R; ++r) {
+                DMat& Mr = gm(*d->ranks[r]);
+                double* dst = gv(*d->ranks[r]) + Mr.n_own;
+                for (int q = 0; q < d->R; ++q) {
+                    if (q == r) continue;
+                    DMat& Mq = gm(*d->ranks[q]);
+                    const int cnt = Mr.recv_off[q + 1] - Mr.recv_off[q];
+                    require(cnt == Mq.send_off[r + 1] - Mq.send_off[r], "dist: inconsistent halo plan");
+                    if (!cnt) continue;
+                    NK(N.send(Mq.send_buf.p + Mq.send_off[r], (size_t)cnt, ncclDouble, c->rank, comm, s));
+                    NK(N.recv(dst + Mr.recv_off[q], (size_t)cnt, ncclDouble, c->rank, comm, s));
+                }
+            }
+            NK(N.groupEnd());
+            return;
+        }
         for (int r = 0; r < d->R; ++r) {
             DMat& Mr = gm(*d->ranks[r]);
             double* dst = gv(*d->ranks[r]) + Mr.n_own;
@@ -664,7 +687,10 @@ Dist* dist_create(Ctx* c, Mat* A, int kind, Hier* h, const int* owner0, int virt
     d->A = A;
     d->h = kind == IBMGPU_PC_SA ? h : nullptr;
     d->kind = kind;
-    d->loop = c->nccl == nullptr;
+    // a one-rank NCCL communicator with virtual ranks runs the loopback decomposition with its
+    // halos moved by NCCL send/recv (the p2p path exercised on a single GPU)
+    d->loop = c->nccl == nullptr || (c->nranks == 1 && virtual_ranks > 1);
+    d->loop_nccl = d->loop && c->nccl != nullptr;
     d->R = d->loop ? std::max(1, virtual_ranks) : c->nranks;
     require(!d->loop || d->R <= kMaxLoop, "dist: at most 16 loopback ranks");
     const int R = d->R;
@@ -890,7 +916,7 @@ void dist_info(const Dist* d, int* info8) {
     const RankData& rk = *d->ranks[0];
     info8[0] = d->R;
     info8[1] = d->D;
-    info8[2] = d->loop ? 1 : 0;
+    info8[2] = d->loop_nccl ? 2 : d->loop ? 1 : 0;
     info8[3] = rk.n_own;
     info8[4] = rk.A.n_halo;
     info8[5] = (int)d->ranks.size();

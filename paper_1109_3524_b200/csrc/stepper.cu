@@ -559,11 +559,15 @@ struct ibmgpu_stepper {
         return own;
     }
 
+    // one process per GPU over NCCL; otherwise virtual ranks on this GPU (loopback, with a
+    // one-rank NCCL communicator moving the halos by NCCL send/recv to self)
+    bool multi_rank() const { return c->nccl && c->nranks > 1; }
+
     void ensure_dist1() {
         if (dist1) return;
-        const int R = c->nccl ? c->nranks : dist_ranks;
+        const int R = multi_rank() ? c->nranks : dist_ranks;
         const auto own = q_owner(R);
-        dist1 = dist_create(c, A, IBMGPU_PC_DIAGONAL, nullptr, own.data(), c->nccl ? 1 : dist_ranks, 0);
+        dist1 = dist_create(c, A, IBMGPU_PC_DIAGONAL, nullptr, own.data(), multi_rank() ? 1 : dist_ranks, 0);
         b1.alloc(c, (size_t)n_q);
         x1.alloc(c, (size_t)n_q);
     }
@@ -572,9 +576,9 @@ struct ibmgpu_stepper {
         if (!dist_stale && dist) return;
         dist_destroy(dist);
         dist = nullptr;
-        const int R = c->nccl ? c->nranks : dist_ranks;
+        const int R = multi_rank() ? c->nranks : dist_ranks;
         const auto own = lambda_owner(R);
-        dist = dist_create(c, lhs2, IBMGPU_PC_SA, hier, own.data(), c->nccl ? 1 : dist_ranks, dist_min_rows);
+        dist = dist_create(c, lhs2, IBMGPU_PC_SA, hier, own.data(), multi_rank() ? 1 : dist_ranks, dist_min_rows);
         if (b2.n != (size_t)n_lambda) {
             b2.alloc(c, (size_t)n_lambda);
             x2.alloc(c, (size_t)n_lambda);
@@ -1161,8 +1165,8 @@ int ibmgpu_stepper_vorticity(ibmgpu_stepper_t S, double* out, int* n) {
 int ibmgpu_stepper_distribute(ibmgpu_stepper_t S, int virtual_ranks, int min_dist_rows) {
     return sguard(S, [&] {
         require(virtual_ranks >= 0, "stepper_distribute: virtual_ranks must be >= 0");
-        require(!S->c->nccl || virtual_ranks <= 1, "stepper_distribute: virtual ranks need a context without NCCL");
-        S->dist_ranks = S->c->nccl ? S->c->nranks : virtual_ranks;
+        require(!S->multi_rank() || virtual_ranks <= 1, "stepper_distribute: virtual ranks need a single-rank context");
+        S->dist_ranks = S->multi_rank() ? S->c->nranks : virtual_ranks;
         S->dist_min_rows = min_dist_rows;
         S->dist_stale = true;
         dist_destroy(S->dist);

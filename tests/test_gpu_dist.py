@@ -157,3 +157,31 @@ def test_nccl_backend_one_rank(small):
         assert ra.ok and rb.ok and abs(ra.solve2_iters - rb.solve2_iters) <= 2
     la, lb = ref.get("lambda"), st.get("lambda")
     assert np.linalg.norm(la - lb) <= 1e-6 * np.linalg.norm(la)
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_nccl_p2p_halos_match_device_copies(small, R):
+    """The ncclSend/ncclRecv halo path on one GPU: a one-rank communicator with R virtual ranks
+    moves every halo as NCCL send/recv pairs to self (captured in the per-iteration graph). The
+    result must be bitwise the device-copy loopback's, for the coupled SA solve and for two
+    distributed Stepper steps (both solves)."""
+    d, A, h, single = small
+    nx, ny = int(d["dims"][0]), int(d["dims"][1])
+    owner = ibm.partition_lambda(nx, ny, _cell_j(d["grid_y_faces"], d["body_y"]), R)
+    ref = ibm.DistSolver(A, ibm.SaPreconditioner(h), owner, virtual_ranks=R).solve(d["bench_b"])
+    ctx = ibm.Context(0, nranks=1, rank=0, nccl_id=ibm.nccl_unique_id())
+    A1 = ibm.SparseMatrix.from_host(H.small_mat(d, "lhs2"), ctx=ctx)
+    h1 = ibm.build_sa_hierarchy(A1, ibm.SaOptions(keep_fine_tail=2 * int(d["dims"][4])))
+    ds = ibm.DistSolver(A1, ibm.SaPreconditioner(h1), owner, virtual_ranks=R)
+    info = ds.info()
+    assert info["loopback"] == 2 and info["nranks"] == R and info["halo"] > 0
+    r = ds.solve(d["bench_b"])
+    assert r.iterations == ref.iterations and np.array_equal(r.x, ref.x)
+    sa, sb = ibm.Stepper(H.case("cylinder_re40_smoke")), ibm.Stepper(H.case("cylinder_re40_smoke"), ctx=ctx)
+    sa.distribute(virtual_ranks=R, min_dist_rows=0)
+    sb.distribute(virtual_ranks=R, min_dist_rows=0)
+    for _ in range(2):
+        ra, rb = sa.advance(), sb.advance()
+        assert ra.ok and rb.ok and ra.solve2_iters == rb.solve2_iters
+    for f in ("q", "lambda"):
+        assert np.array_equal(sa.get(f), sb.get(f))
