@@ -102,6 +102,10 @@ int ibmgpu_csr_destroy(ibmgpu_ctx_t ctx, ibmgpu_mat_t m);
 int ibmgpu_spmv(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, const double* x_dev, double* y_dev);
 /* SparseMatrix::spmv (sparse.hpp:112-118) with host vectors (H2D, SpMV, D2H) */
 int ibmgpu_spmv_host(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, const double* x_host, double* y_host);
+/* benchmark helper (no reference counterpart): `reps` back-to-back y = A x launches captured in one
+ * CUDA graph (programmatic dependent launch between them), timed warm with events; *us_per_launch */
+int ibmgpu_spmv_timed(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, const double* x_dev, double* y_dev, int reps,
+                      double* us_per_launch);
 /* SparseMatrix::transpose (sparse.hpp:120-138) */
 int ibmgpu_transpose(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, ibmgpu_mat_t* out);
 /* spmm (sparse.hpp:270) — Gustavson order, cancelled entries kept */

@@ -84,6 +84,7 @@ _SIGS = [
     ("ibmgpu_csr_destroy", C.c_int, [_vp, _vp]),
     ("ibmgpu_spmv", C.c_int, [_vp, _vp, _dp, _dp]),
     ("ibmgpu_spmv_host", C.c_int, [_vp, _vp, _dp, _dp]),
+    ("ibmgpu_spmv_timed", C.c_int, [_vp, _vp, _dp, _dp, C.c_int, _dp]),
     ("ibmgpu_transpose", C.c_int, [_vp, _vp, C.POINTER(_vp)]),
     ("ibmgpu_spmm", C.c_int, [_vp, _vp, _vp, C.POINTER(_vp)]),
     ("ibmgpu_triple_product", C.c_int, [_vp, _vp, _vp, _vp, C.c_int, C.POINTER(_vp), C.POINTER(C.c_longlong), _ip]),
@@ -155,7 +156,10 @@ def load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise FileNotFoundError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build())")
     lib = C.CDLL(LIB_PATH)
+    override = "IBMGPU_LIB" in os.environ  # A/B runs may load an older build missing newer entries
     for name, res, args in _SIGS:
+        if override and not hasattr(lib, name):
+            continue
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args

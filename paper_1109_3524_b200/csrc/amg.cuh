@@ -11,6 +11,8 @@
 // L.omega * L.inv_diag[i] (amg.hpp:210, :224); SELL levels therefore reproduce v_cycle bit for bit
 // up to the coarse solve.
 #pragma once
+#include <algorithm>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -192,7 +194,12 @@ inline void vcycle_launch(Ctx* c, Hier* h, const double* r_in, double* z_out, co
         coarse_solve(c, h, r_in, z_out, done, s);
         return;
     }
-    const int F = h->n_phases ? h->fuse_from : L;  // levels >= F run inside the fused kernel
+    int F = h->n_phases ? h->fuse_from : L;  // levels >= F run inside the fused kernel
+    // IBMGPU_DEBUG_VDEPTH=k (timing experiments only; results are wrong): run levels < k and no
+    // coarse solve unless k > L, to measure each level's in-graph cost by difference
+    static const int vdepth = std::getenv("IBMGPU_DEBUG_VDEPTH") ? std::atoi(std::getenv("IBMGPU_DEBUG_VDEPTH")) : 0;
+    const bool truncated = vdepth > 0 && vdepth <= L;
+    if (truncated) F = std::min(F, vdepth);
     for (int l = 0; l < F; ++l) {
         Level& lv = *h->levels[l];
         const double* b = l == 0 ? r_in : lv.b.p;
@@ -209,7 +216,8 @@ inline void vcycle_launch(Ctx* c, Hier* h, const double* r_in, double* z_out, co
             launch_spmv(c, lv.Pt, XPlain{lv.r.p}, EpiStoreSkip{h->cb.p, done}, s);
         }
     }
-    if (F < L) {
+    if (truncated) {
+    } else if (F < L) {
         k_coarse_cycle<<<h->coarse_grid, kBlock, 0, s>>>(CoarsePlan{h->phases.p, h->n_phases, h->bar.p, h->bar.p + 1},
                                                          done);
         CK_LAUNCH(c);

@@ -205,6 +205,35 @@ int ibmgpu_spmv(ibmgpu_ctx_t c, ibmgpu_mat_t A, const double* x, double* y) {
     });
 }
 
+int ibmgpu_spmv_timed(ibmgpu_ctx_t c, ibmgpu_mat_t A, const double* x, double* y, int reps, double* us) {
+    return guard(c, [&] {
+        need(A && x && y && us && reps > 0, "spmv_timed: bad argument");
+        if (!A->planned) mat_plan(c, A);
+        spmv(c, A, x, y);  // warm: plan buffers, instruction cache
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < reps; ++i) spmv(c, A, x, y);
+        CK(cudaStreamEndCapture(c->stream, &g));
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaGraphLaunch(ge, c->stream));
+        CK(cudaEventRecord(e0, c->stream));
+        CK(cudaGraphLaunch(ge, c->stream));
+        CK(cudaEventRecord(e1, c->stream));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        *us = 1e3 * ms / reps;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+    });
+}
+
 int ibmgpu_spmv_host(ibmgpu_ctx_t c, ibmgpu_mat_t A, const double* x, double* y) {
     return guard(c, [&] {
         need(A != nullptr, "spmv: null matrix");

@@ -265,8 +265,8 @@ __global__ void __launch_bounds__(128) k_symv_tiles(int n, int nt, const double*
                      : "memory");
     }
     pdl_wait();
-    const bool skip = done && *(volatile const int*)done;
-    if (!skip && threadIdx.x < TS) {
+    const bool skip = done && *(volatile const int*)done;  // x is read regardless: one round trip
+    if (threadIdx.x < TS) {
         const int gi = I * TS + threadIdx.x, gj = J * TS + threadIdx.x;
         xi[threadIdx.x] = gi < n ? x[gi] : 0.0;
         xj[threadIdx.x] = gj < n ? x[gj] : 0.0;
@@ -297,12 +297,13 @@ __global__ void __launch_bounds__(128) k_symv_tiles(int n, int nt, const double*
 __global__ void k_symv_combine(int n, int nt, const double* __restrict__ prow, const double* __restrict__ pcol,
                                double* __restrict__ y, const int* done) {
     pdl_wait();
-    if (done && *(volatile const int*)done) return;
+    const bool skip = done && *(volatile const int*)done;  // tested after the partial loads
     const int I = blockIdx.x, r = threadIdx.x;
     if (r >= TS) return;
     double s = 0.0;
     for (int J = 0; J <= I; ++J) s += prow[((size_t)I * (I + 1) / 2 + J) * TS + r];
     for (int K = I + 1; K < nt; ++K) s += pcol[((size_t)K * (K + 1) / 2 + I) * TS + r];
+    if (skip) return;
     const int gi = I * TS + r;
     if (gi < n) y[gi] = s;
     pdl_release();

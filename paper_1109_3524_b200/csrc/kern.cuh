@@ -148,7 +148,9 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Epi epi, int nblocks) 
     constexpr int NR = Epi::NR;
     constexpr int U = 8;
     pdl_wait();
-    if (epi.skip()) return;
+    // the done flag is read alongside the partials (one L2 round trip, not two); a converged
+    // solve skips only the epilogue
+    const bool skip = epi.skip();
     const RedSlot slot = epi.slot();
     double t[NR];
 #pragma unroll
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Epi epi, int nblocks) 
 #pragma unroll
         for (int r = 0; r < NR; ++r) t[r] += slot.partials[(size_t)b * NR + r];
     block_sum<NR>(t);
-    if (threadIdx.x == 0) epi.fin(t);
+    if (!skip && threadIdx.x == 0) epi.fin(t);
 }
 
 // ---------------------------------------------------------------- operand gathers
@@ -231,7 +233,8 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
                 a[q][u] = __ldg(v + base[q] + 32 * u);
             }
     pdl_wait();
-    if (epi.skip()) return;
+    // the done flag load overlaps the gathers; nothing is written before it is tested
+    const bool skip = epi.skip();
     if constexpr (requires { epi.touch(0); }) {
 #pragma unroll
         for (int q = 0; q < kSellRows; ++q)
@@ -247,6 +250,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
         for (int k = kSellU; k < len[q]; ++k)  // rows wider than kSellU (body-coupled rows)
             s[q] = addd(s[q], mul(__ldg(v + base[q] + 32 * k), xf(__ldg(ci + base[q] + 32 * k))));
     }
+    if (skip) return;
 #pragma unroll
     for (int q = 0; q < kSellRows; ++q)
         if (ix[q] < rows) epi.row(ix[q], s[q], acc);
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_stencil(int rows, StencilPla
             if (m & (1u << q)) a[q] = __ldg(P.v + (size_t)q * rows + i);
     }
     pdl_wait();
-    if (epi.skip()) return;
+    const bool skip = epi.skip();  // tested after the gathers are issued
     if constexpr (requires { epi.touch(0); }) {
         if (live) epi.touch(i);
     }
@@ -321,6 +325,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_stencil(int rows, StencilPla
             for (int k = __ldg(P.erp + i); k < e; ++k) s = addd(s, mul(__ldg(P.ev + k), xf(__ldg(P.eci + k))));
         }
     }
+    if (skip) return;
     if (live) epi.row(i, s, acc);
     pdl_release();
     if constexpr (NR > 0) {
@@ -375,15 +380,17 @@ __global__ void __launch_bounds__(kBlock, kU == 4 ? 4 : 2) k_spmv_sellw(int rows
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
     if (blockIdx.x >= sblocks) {
-        pdl_wait();
-        if (epi.skip()) return;
         const int w = (blockIdx.x - sblocks) * (kBlock / 32) + (threadIdx.x >> 5);
         const int lane = threadIdx.x & 31;
-        if (w < n_long) {
-            const int row = __ldg(long_rows + w);
+        const int row = w < n_long ? __ldg(long_rows + w) : -1;  // plan data: before the wait
+        pdl_wait();
+        const bool skip = epi.skip();
+        if (row >= 0) {
             const double s = row_sum_inorder(row, rp, csr_ci, csr_v, xf, lane);  // CSR arrays, not the slices
+            if (skip) return;
             if (lane == 0) epi.row(row, s, acc);
         }
+        if (skip) return;
         pdl_release();
         if constexpr (NR > 0) block_partial<NR>(acc, epi.slot());
         return;
@@ -405,7 +412,7 @@ __global__ void __launch_bounds__(kBlock, kU == 4 ? 4 : 2) k_spmv_sellw(int rows
             a0[u] = __ldg(v + base + 32 * u);
         }
     pdl_wait();  // everything above is the (constant) matrix
-    if (epi.skip()) return;
+    const bool skip = epi.skip();
     if constexpr (requires { epi.touch(0); }) {
         if (row >= 0) epi.touch(row);
     }
@@ -428,6 +435,7 @@ __global__ void __launch_bounds__(kBlock, kU == 4 ? 4 : 2) k_spmv_sellw(int rows
             a0[u] = a1[u];
         }
     }
+    if (skip) return;
     if (row >= 0) epi.row(row, s, acc);
     pdl_release();
     if constexpr (NR > 0) {
@@ -452,7 +460,10 @@ struct AdaptPlan {
 };
 
 template <class XF, class Epi>
-__global__ void __launch_bounds__(kBlock) k_spmv_adapt(AdaptPlan pl, const int* __restrict__ rp,
+#ifndef IBMGPU_ADAPT_MINB
+#define IBMGPU_ADAPT_MINB 8
+#endif
+__global__ void __launch_bounds__(kBlock, IBMGPU_ADAPT_MINB) k_spmv_adapt(AdaptPlan pl, const int* __restrict__ rp,
                                                        const int* __restrict__ ci, const double* __restrict__ v,
                                                        XF xf, Epi epi) {
     constexpr int NR = Epi::NR;
@@ -462,26 +473,29 @@ __global__ void __launch_bounds__(kBlock) k_spmv_adapt(AdaptPlan pl, const int* 
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
     const int tpr = m.z;
     if (tpr == 0) {  // one chunk of a long row, whole CTA
-        pdl_wait();
-        if (epi.skip()) return;
         const int row = m.x, chunk = m.y;
         const int2 lr = __ldg(pl.lrow + m.w);
         const int kb = __ldg(rp + row) + chunk * kRowChunk;
         const int e = min(kb + kRowChunk, __ldg(rp + row + 1));
+        pdl_wait();
+        const bool skip = epi.skip();
         double s = 0.0;
         int k = kb + threadIdx.x;
         for (; k + 3 * kBlock < e; k += 4 * kBlock) {  // 4 independent gathers in flight per thread
             int c[4];
-            double a[4];
+            double a[4], xv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 c[u] = __ldg(ci + k + u * kBlock);
                 a[u] = __ldg(v + k + u * kBlock);
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) s = addd(s, mul(a[u], xf(c[u])));
+            for (int u = 0; u < 4; ++u) xv[u] = xf(c[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s = addd(s, mul(a[u], xv[u]));
         }
         for (; k < e; k += kBlock) s = addd(s, mul(__ldg(v + k), xf(__ldg(ci + k))));
+        if (skip) return;
         double t[1] = {s};
         block_sum<1>(t);
         if (threadIdx.x == 0) {
@@ -520,7 +534,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_adapt(AdaptPlan pl, const int* 
             load_batch();
         }
         pdl_wait();
-        if (epi.skip()) return;
+        const bool skip = epi.skip();  // tested once the first pass's gathers are in flight
         for (int base = r0; base < r1; base += ngrp) {
             i = base + grp;
             double s = 0.0;
@@ -531,17 +545,28 @@ __global__ void __launch_bounds__(kBlock) k_spmv_adapt(AdaptPlan pl, const int* 
                     load_batch();
                 }
                 // predicated 4-wide batches: a lane's last (partial) batch issues all its loads at
-                // once instead of one dependent index->gather chain per remaining entry
+                // once instead of one dependent index->gather chain per remaining entry. All four
+                // gathers issue before the first add, and the next batch's indices/values are
+                // requested while they are in flight.
                 for (;;) {
+                    double xv[4], av[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        xv[u] = k + u * tpr < e ? xf(c[u]) : 0.0;
+                        av[u] = a[u];
+                    }
+                    const int kc = k;
+                    k += 4 * tpr;
+                    const bool more = k < e;
+                    if (more) load_batch();
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
-                        if (k + u * tpr < e) s = addd(s, mul(a[u], xf(c[u])));
-                    k += 4 * tpr;
-                    if (k >= e) break;
-                    load_batch();
+                        if (kc + u * tpr < e) s = addd(s, mul(av[u], xv[u]));
+                    if (!more) break;
                 }
             }
             for (int o = tpr >> 1; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o, tpr);
+            if (skip) return;
             if (i < r1 && lane == 0) epi.row(i, s, acc);
         }
     }
