@@ -141,6 +141,9 @@ int ibmgpu_amg_solve(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, ibmgpu_hier_t h, const do
                      const ibm_solver_params* params, ibm_solve_result* result);
 /* SaHierarchy inspection (amg.hpp:33-52): levels, coarsening_stalled, coarse size */
 int ibmgpu_hier_info(ibmgpu_hier_t h, int* n_levels, int* stalled, int* coarse_rows);
+/* device-only (no reference counterpart): how many of the last levels the V-cycle applies as one
+ * folded dense operator, and its dimension (0 and coarse_rows when nothing is folded; fold.cu) */
+int ibmgpu_hier_folded(ibmgpu_hier_t h, int* n_fold, int* dense_rows);
 /* level l: borrowed handles (valid while h lives) and omega; l == n_levels gives coarse_A in *A */
 int ibmgpu_hier_level(ibmgpu_hier_t h, int l, ibmgpu_mat_t* A, ibmgpu_mat_t* P, ibmgpu_mat_t* Pt, double* omega);
 /* aggregate ids of level l's core rows (sa_detail::aggregate, amg.hpp:79-107); returns count */

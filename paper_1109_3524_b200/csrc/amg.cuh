@@ -49,7 +49,12 @@ struct ibmgpu_hier {
     int n_c = 0;
     ibmgpu::DBuf<double> coarse_inv;  // n_c x n_c row-major, symmetric
     ibmgpu::DBuf<double> coarse_tiles, prow, pcol;  // packed lower-triangle tiles + SYMV partials
-    ibmgpu::DBuf<double> cb, cx;      // coarse rhs / solution
+    ibmgpu::DBuf<double> cb, cx;      // coarse rhs / solution (n_dense)
+    // fold.cu: the last n_fold levels folded into one dense operator of dimension n_dense (the
+    // coarse solve then applies it; n_fold = 0: n_dense = n_c, the coarse inverse itself)
+    int n_fold = 0, n_dense = 0;
+    ibmgpu::DBuf<double> dense;       // n_dense x n_dense row-major (freed once packed)
+    int active_levels() const { return (int)levels.size() - n_fold; }
     // fused coarse sub-cycle (coarse.cuh): levels [fuse_from, L) + dense solve in one launch
     int fuse_from = 0;
     int n_phases = 0, coarse_grid = 0;
@@ -72,6 +77,9 @@ void dense_spd_inverse(Ctx* c, const Mat* Ac, double* inv);  // factor (dense.hp
 void launch_dense_gemv(Ctx* c, int n, const double* Ainv, const double* x, double* y, const int* done,
                        cudaStream_t s);
 void pack_symmetric_tiles(Ctx* c, int n, const double* full, double* tiles);
+constexpr int kSymvTile = 64;  // packed SYMV tile edge (dense.cu)
+// fold.cu
+void fold_tail(Ctx* c, Hier* h, int tile);
 size_t packed_tiles_doubles(int n);
 size_t packed_partials_doubles(int n);
 void launch_symv_packed(Ctx* c, int n, const double* tiles, const double* x, double* y, double* prow, double* pcol,
@@ -79,7 +87,7 @@ void launch_symv_packed(Ctx* c, int n, const double* tiles, const double* x, dou
 
 // coarsest level: y = A_c^{-1} x from the packed symmetric inverse (each element read once)
 inline void coarse_solve(Ctx* c, Hier* h, const double* x, double* y, const int* done, cudaStream_t s) {
-    launch_symv_packed(c, h->n_c, h->coarse_tiles.p, x, y, h->prow.p, h->pcol.p, done, s);
+    launch_symv_packed(c, h->n_dense, h->coarse_tiles.p, x, y, h->prow.p, h->pcol.p, done, s);
 }
 
 // ---------------------------------------------------------------- V-cycle epilogues
@@ -189,7 +197,7 @@ struct EpiPostSmoothDot {
 template <class LastEpi>
 inline void vcycle_launch(Ctx* c, Hier* h, const double* r_in, double* z_out, const int* done, LastEpi last,
                           cudaStream_t s) {
-    const int L = (int)h->levels.size();
+    const int L = h->active_levels();
     if (L == 0) {
         coarse_solve(c, h, r_in, z_out, done, s);
         return;
@@ -250,8 +258,8 @@ struct LastPlain {
 // kernels launched by one V-cycle (for launch accounting)
 inline int vcycle_kernels(const Hier* h) {
     if (h->levels.empty()) return 1;
-    const int F = h->n_phases ? h->fuse_from : (int)h->levels.size();
-    return 4 * F + 1;
+    const int F = h->n_phases ? h->fuse_from : h->active_levels();
+    return 4 * F + 2;  // + the two SYMV kernels
 }
 
 }  // namespace ibmgpu

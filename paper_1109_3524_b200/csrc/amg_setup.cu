@@ -628,14 +628,23 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
         clk.lap("plans", -1);
         h->coarse_inv.alloc(c, (size_t)h->n_c * h->n_c);
         dense_spd_inverse(c, h->coarse_A, h->coarse_inv.p);
-        h->coarse_tiles.alloc(c, packed_tiles_doubles(h->n_c));
-        h->prow.alloc(c, packed_partials_doubles(h->n_c));
-        h->pcol.alloc(c, packed_partials_doubles(h->n_c));
-        pack_symmetric_tiles(c, h->n_c, h->coarse_inv.p, h->coarse_tiles.p);
-        h->cb.alloc(c, (size_t)h->n_c);
-        h->cx.alloc(c, (size_t)h->n_c);
-        build_fused_coarse(c, h);
         clk.lap("coarse", -1);
+        h->n_dense = h->n_c;
+        fold_tail(c, h, kSymvTile);
+        clk.lap("fold", -1);
+        const int nd = h->n_dense;
+        h->coarse_tiles.alloc(c, packed_tiles_doubles(nd));
+        h->prow.alloc(c, packed_partials_doubles(nd));
+        h->pcol.alloc(c, packed_partials_doubles(nd));
+        pack_symmetric_tiles(c, nd, h->n_fold ? h->dense.p : h->coarse_inv.p, h->coarse_tiles.p);
+        h->cb.alloc(c, (size_t)nd);
+        h->cx.alloc(c, (size_t)nd);
+        if (h->n_fold) {
+            h->dense.release();
+            h->coarse_inv.release();
+        } else {
+            build_fused_coarse(c, h);
+        }
         sync(c);
     } catch (...) {
         delete h;

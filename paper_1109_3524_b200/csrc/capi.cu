@@ -321,6 +321,13 @@ int ibmgpu_hier_info(ibmgpu_hier_t h, int* n_levels, int* stalled, int* coarse_r
     return 0;
 }
 
+int ibmgpu_hier_folded(ibmgpu_hier_t h, int* n_fold, int* dense_rows) {
+    if (!h) return IBMGPU_EINVAL;
+    if (n_fold) *n_fold = h->n_fold;
+    if (dense_rows) *dense_rows = h->n_dense;
+    return 0;
+}
+
 int ibmgpu_hier_level(ibmgpu_hier_t h, int l, ibmgpu_mat_t* A, ibmgpu_mat_t* P, ibmgpu_mat_t* Pt, double* omega) {
     if (!h || l < 0 || l > (int)h->levels.size()) return IBMGPU_EINVAL;
     if (l == (int)h->levels.size()) {

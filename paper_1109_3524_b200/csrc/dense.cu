@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(256) k_gemv(int n, const double* __restrict__ 
 }
 
 // ---- packed symmetric inverse: lower-triangle 64x64 tiles, tile (I,J), J <= I, at I(I+1)/2+J
-constexpr int TS = 64;
+constexpr int TS = kSymvTile;
 constexpr int TP = TS + 1;  // stored row pitch of a packed tile: the pad keeps row and column reads
                             // of the smem copy bank-conflict free, and lets one bulk copy land it
 

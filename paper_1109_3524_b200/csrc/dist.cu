@@ -496,7 +496,7 @@ void allreduce(Dist* d, GetV gv, int n) {
 
 // Replicated tail: V-cycle from level D (full vectors, amg.cuh kernels) — b_in -> out.
 void vcycle_from(Ctx* c, Hier* h, int D, const double* b_in, double* out, const int* done, cudaStream_t s) {
-    const int L = (int)h->levels.size();
+    const int L = h->active_levels();
     if (D == L) {
         coarse_solve(c, h, b_in, out, done, s);
         return;
@@ -699,7 +699,7 @@ Dist* dist_create(Ctx* c, Mat* A, int kind, Hier* h, const int* owner0, int virt
     d->owner.emplace_back(owner0, owner0 + n);
     for (int o : d->owner[0]) require(o >= 0 && o < R, "dist: owner out of range");
     if (d->h) {
-        const int L = (int)h->levels.size();
+        const int L = h->active_levels();  // folded tail levels are part of the dense coarse solve
         if (L == 0) fail(IBMGPU_ESUPPORT, "dist: hierarchy has no levels to distribute");
         require(h->levels[0]->A->rows == n, "dist: hierarchy size does not match the matrix");
         int D = 0;
@@ -735,7 +735,7 @@ Dist* dist_create(Ctx* c, Mat* A, int kind, Hier* h, const int* owner0, int virt
             v = 1.0 / v;
         }
     }
-    const int nD = d->h ? (d->D < (int)h->levels.size() ? h->levels[d->D]->A->rows : h->n_c) : 0;
+    const int nD = d->h ? (d->D < h->active_levels() ? h->levels[d->D]->A->rows : h->n_dense) : 0;
     std::vector<int> local_ranks;
     if (d->loop)
         for (int r = 0; r < R; ++r) local_ranks.push_back(r);

@@ -338,6 +338,12 @@ class SaHierarchy:
         self.ctx.lib.ibmgpu_hier_info(self.h, C.byref(nl), C.byref(st), C.byref(nc))
         return nl.value, bool(st.value), nc.value
 
+    def folded(self) -> tuple[int, int]:
+        """(levels folded into the dense coarse operator, its dimension) — fold.cu"""
+        nf, nd = C.c_int(), C.c_int()
+        self.ctx.check(self.ctx.lib.ibmgpu_hier_folded(self.h, C.byref(nf), C.byref(nd)))
+        return nf.value, nd.value
+
     @property
     def n_levels(self) -> int:
         return self.info()[0]

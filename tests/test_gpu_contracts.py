@@ -106,3 +106,27 @@ def test_zero_state_stays_bitwise_zero():
         assert not np.any(st.get("q")) and not np.any(st.get("lambda"))
     finally:
         os.unlink(path)
+
+
+def test_folded_tail_is_the_same_operator(monkeypatch):
+    """fold.cu: the smallest levels applied as one dense operator M_l = 2W - WAW + B^T M_{l+1} B
+    give the V-cycle of the unfolded hierarchy to rounding, and the same PCG iterations."""
+    import bench
+    cfg, h_min, dt, _ = bench.workload("c2")
+    st = ibm.Stepper(H.case(cfg), h_min=h_min, dt=dt)
+    A = st.op("lhs2")
+    opts = ibm.SaOptions(keep_fine_tail=2 * st.n_b)
+    monkeypatch.setenv("IBMGPU_FOLD", "0")
+    h0 = ibm.build_sa_hierarchy(A, opts)
+    monkeypatch.setenv("IBMGPU_FOLD", "1")
+    h1 = ibm.build_sa_hierarchy(A, opts)
+    assert h0.folded() == (0, h0.info()[2])
+    nf, nd = h1.folded()
+    assert nf >= 1 and nd == h1.level(h1.n_levels - nf)["A"].rows()
+    assert h1.n_levels == h0.n_levels and h1.info()[2] == h0.info()[2]  # the reference structure is kept
+    b = H.bench_rhs(A.spmv, A.rows())
+    z0, z1 = ibm.sa_apply(h0, b), ibm.sa_apply(h1, b)
+    assert np.linalg.norm(z1 - z0) <= 1e-13 * np.linalg.norm(z0)
+    r0 = ibm.pcg(A, b, None, ibm.SaPreconditioner(h0), ibm.SolverParams())
+    r1 = ibm.pcg(A, b, None, ibm.SaPreconditioner(h1), ibm.SolverParams())
+    assert r0.iterations == r1.iterations and np.max(np.abs(r1.x - r0.x)) <= 1e-9 * np.max(np.abs(r0.x))
