@@ -241,6 +241,7 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast
 __global__ void __launch_bounds__(128) k_symv_tiles(int n, int nt, const double* __restrict__ tiles,
                                                     const double* __restrict__ x, double* __restrict__ prow,
                                                     double* __restrict__ pcol, const int* done) {
+    pdl_release_early(6);
     __shared__ alignas(128) double A[TS][TP];
     __shared__ double xi[TS], xj[TS];
     __shared__ alignas(8) unsigned long long bar;
@@ -290,12 +291,13 @@ __global__ void __launch_bounds__(128) k_symv_tiles(int n, int nt, const double*
         for (int k = 0; k < TS; ++k) s += A[k][cc] * xi[k];
         pcol[(size_t)t * TS + cc] = s;
     }
-    pdl_release();
+    pdl_release_late(6);
 }
 
 // y_I = sum_{J<=I} prow[(I,J)] + sum_{K>I} pcol[(K,I)], fixed order
 __global__ void k_symv_combine(int n, int nt, const double* __restrict__ prow, const double* __restrict__ pcol,
                                double* __restrict__ y, const int* done) {
+    pdl_release_early(8);
     pdl_wait();
     const bool skip = done && *(volatile const int*)done;  // tested after the partial loads
     const int I = blockIdx.x, r = threadIdx.x;
@@ -306,7 +308,7 @@ __global__ void k_symv_combine(int n, int nt, const double* __restrict__ prow, c
     if (skip) return;
     const int gi = I * TS + r;
     if (gi < n) y[gi] = s;
-    pdl_release();
+    pdl_release_late(8);
 }
 
 }  // namespace

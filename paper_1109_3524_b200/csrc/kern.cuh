@@ -31,6 +31,19 @@ __device__ __forceinline__ void pf(const void* p) { asm volatile("prefetch.globa
 // kernel's launch and CTA rasterisation overlap this kernel's tail instead of following it.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+// Grids that fit in one wave release their dependents as soon as every CTA has started, so the
+// next kernel's CTAs become resident and stream their (constant) matrix data while this kernel
+// runs; larger grids release at the end of each CTA (early dependents would take the slots of
+// this grid's later waves).
+// `bps` is the kernel's resident CTAs per SM (its launch bounds); 148 SMs on B200.
+constexpr int kNumSms = 148;
+__device__ __forceinline__ bool pdl_early(int bps) { return gridDim.x <= kNumSms * bps; }
+__device__ __forceinline__ void pdl_release_early(int bps) {
+    if (pdl_early(bps)) pdl_release();
+}
+__device__ __forceinline__ void pdl_release_late(int bps) {
+    if (!pdl_early(bps)) pdl_release();
+}
 
 inline bool pdl_enabled() {
     static const bool on = [] {
@@ -145,6 +158,7 @@ constexpr int kFinThreads = 1024;
 
 template <class Epi>
 __global__ void __launch_bounds__(kFinThreads) k_finalize(Epi epi, int nblocks) {
+    pdl_release_early(1);
     constexpr int NR = Epi::NR;
     constexpr int U = 8;
     pdl_wait();
@@ -202,6 +216,7 @@ template <class XF, class Epi>
 __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __restrict__ rp,
                                                          const int* __restrict__ off, const int* __restrict__ ci,
                                                          const double* __restrict__ v, XF xf, Epi epi) {
+    pdl_release_early(8);
     constexpr int NR = Epi::NR;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
@@ -254,7 +269,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
 #pragma unroll
     for (int q = 0; q < kSellRows; ++q)
         if (ix[q] < rows) epi.row(ix[q], s[q], acc);
-    pdl_release();
+    pdl_release_late(8);
     if constexpr (NR > 0) {
         block_partial<NR>(acc, epi.slot());
     }
@@ -276,6 +291,7 @@ struct StencilPlan {
 
 template <class XF, class Epi>
 __global__ void __launch_bounds__(kBlock, 8) k_spmv_stencil(int rows, StencilPlan P, XF xf, Epi epi) {
+    pdl_release_early(8);
     constexpr int NR = Epi::NR;
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
@@ -327,7 +343,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_stencil(int rows, StencilPla
     }
     if (skip) return;
     if (live) epi.row(i, s, acc);
-    pdl_release();
+    pdl_release_late(8);
     if constexpr (NR > 0) {
         block_partial<NR>(acc, epi.slot());
     }
@@ -374,6 +390,7 @@ __global__ void __launch_bounds__(kBlock, kU == 4 ? 4 : 2) k_spmv_sellw(int rows
                                                           XF xf, Epi epi, int sblocks, const int* __restrict__ long_rows,
                                                           int n_long, const int* __restrict__ csr_ci,
                                                           const double* __restrict__ csr_v) {
+    pdl_release_early(kU == 4 ? 4 : 2);
     constexpr int NR = Epi::NR;
     constexpr int U = kU;
     double acc[NR > 0 ? NR : 1];
@@ -391,7 +408,7 @@ __global__ void __launch_bounds__(kBlock, kU == 4 ? 4 : 2) k_spmv_sellw(int rows
             if (lane == 0) epi.row(row, s, acc);
         }
         if (skip) return;
-        pdl_release();
+        pdl_release_late(kU == 4 ? 4 : 2);
         if constexpr (NR > 0) block_partial<NR>(acc, epi.slot());
         return;
     }
@@ -437,7 +454,7 @@ __global__ void __launch_bounds__(kBlock, kU == 4 ? 4 : 2) k_spmv_sellw(int rows
     }
     if (skip) return;
     if (row >= 0) epi.row(row, s, acc);
-    pdl_release();
+    pdl_release_late(kU == 4 ? 4 : 2);
     if constexpr (NR > 0) {
         block_partial<NR>(acc, epi.slot());
     }
@@ -466,6 +483,7 @@ template <class XF, class Epi>
 __global__ void __launch_bounds__(kBlock, IBMGPU_ADAPT_MINB) k_spmv_adapt(AdaptPlan pl, const int* __restrict__ rp,
                                                        const int* __restrict__ ci, const double* __restrict__ v,
                                                        XF xf, Epi epi) {
+    pdl_release_early(IBMGPU_ADAPT_MINB);
     constexpr int NR = Epi::NR;
     const int4 m = __ldg(pl.meta + blockIdx.x);  // plan and matrix are constant: read before the wait
     double acc[NR > 0 ? NR : 1];
@@ -570,7 +588,7 @@ __global__ void __launch_bounds__(kBlock, IBMGPU_ADAPT_MINB) k_spmv_adapt(AdaptP
             if (i < r1 && lane == 0) epi.row(i, s, acc);
         }
     }
-    pdl_release();
+    pdl_release_late(IBMGPU_ADAPT_MINB);
     if constexpr (NR > 0) {
         block_partial<NR>(acc, epi.slot());
     }
@@ -631,6 +649,7 @@ struct EpiStore {
 // Elementwise kernels over n with an optional fused reduction (same epilogue contract).
 template <class Body>
 __global__ void __launch_bounds__(kBlock) k_elem(int n, Body body) {
+    pdl_release_early(8);
     constexpr int NR = Body::NR;
     pdl_wait();
     if (body.skip()) return;
@@ -638,7 +657,7 @@ __global__ void __launch_bounds__(kBlock) k_elem(int n, Body body) {
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
     for (int i = blockIdx.x * kBlock + threadIdx.x; i < n; i += gridDim.x * kBlock) body.row(i, acc);
-    pdl_release();
+    pdl_release_late(8);
     if constexpr (NR > 0) block_partial<NR>(acc, body.slot());
 }
 
