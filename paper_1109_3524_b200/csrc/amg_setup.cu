@@ -6,7 +6,8 @@
 //                                          pass 1 is the lexicographically-first independent set of
 //                                          the conflict relation N[i] ∩ N[s] ≠ ∅ (N[x] = {x} ∪ out(x)),
 //                                          resolved by a persistent dependency-driven kernel (a node
-//                                          decides once every lower conflicting node has decided);
+//                                          decides once every lower conflicting node has decided) on
+//                                          large levels, by the chunked sequential loop on small ones;
 //                                          pass 2 follows "first already-assigned neighbour in column
 //                                          order" chains by pointer jumping; pass 3 numbers leftovers
 //   spectral radius      amg.hpp:58-75    10 power iterations, LCG start vector by jump-ahead
@@ -122,13 +123,11 @@ __global__ void __launch_bounds__(256) k_lfmis(int n, const int* __restrict__ sr
     }
 }
 
-// Pass 1 for small, dense levels (n <= kSeqMax): the reference's sequential loop itself
-// (amg.hpp:85-95), run by ONE warp with the "assigned" set as a bitmap in shared memory. Lanes test
-// a row's columns in parallel (ballot); rows arrive through a cp.async ring kGD rows ahead, so the
-// loop never waits on DRAM. On the dense coarse levels (50-130 strong neighbours, distance-2
-// conflict sets of thousands) this beats the parallel LFMIS below ~30k rows (flapping L3, 6.3k rows:
-// 1.9 vs 4.4 ms); at 66k rows it is already slower (21 vs 19 ms), so larger levels keep the LFMIS.
-constexpr int kSeqMax = 32768, kGD = 16, kGW = 256, kWin = 1024;
+// Pass 1, the reference's sequential loop itself (amg.hpp:85-95), run by ONE warp with the
+// "assigned" set as a bitmap in shared memory. Lanes test a row's columns in parallel (ballot); rows
+// arrive through a cp.async ring kGD rows ahead. Kept as the plainest restatement (IBMGPU_AGG=seq);
+// k_greedy_chunk below computes the same seeds faster on every level measured.
+constexpr int kGD = 16, kGW = 256, kWin = 1024;
 
 __device__ __forceinline__ void cp_async4(int* dst, const int* src) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -189,6 +188,180 @@ __global__ void __launch_bounds__(32) k_greedy_seq(int n, const int* __restrict_
         issue(i + kGD);  // the slot of row i is free again
     }
     asm volatile("cp.async.wait_all;" ::);
+}
+
+// Pass 1 for dense levels of any size that fit a shared-memory bitmap: the same sequential loop,
+// split so that only its truly serial part is serial. Rows go in chunks of <= kChunk rows whose
+// strong-neighbour lists (contiguous in S) are staged in shared memory by cp.async one chunk ahead.
+//   phase A (32 warps): a row is "covered" if it or a strong neighbour is assigned at chunk start;
+//                       covering only grows, so a row covered now is covered in the reference too;
+//   phase B (warp 0):   the remaining candidates in index order; the first one is a seed outright,
+//                       later ones are re-tested against the bits the chunk's earlier seeds set.
+// Same seeds as k_greedy_seq; on levels with tens of strong neighbours per row most rows are
+// settled in phase A.
+constexpr int kChunk = 1024;
+
+template <bool kLane>
+__global__ void __launch_bounds__(kChunk) k_greedy_chunk(int n, const int* __restrict__ srp,
+                                                         const int* __restrict__ sci, int* __restrict__ status,
+                                                         int cap) {
+    extern __shared__ __align__(16) unsigned csm[];
+    const int nwords = (n + 31) >> 5;
+    unsigned* bits = csm;
+    int* rpb = reinterpret_cast<int*>(bits + ((nwords + 3) & ~3));  // [2][kChunk + 1] row pointers
+    int* cflag = rpb + 2 * (kChunk + 4);                             // [kChunk] candidate flags
+    int* meta = cflag + kChunk;                                      // [2][4]: base, end, aligned start
+    int* buf = meta + 8;                                             // [2][cap] column lists
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    for (int k = t; k < nwords; k += kChunk) bits[k] = 0u;
+
+    // bounds of the chunk starting at `base` and its loads into slot `sl`; one commit group per call
+    auto stage = [&](int base, int sl) {
+        int* rpw = rpb + sl * (kChunk + 4);
+        int* m = meta + 4 * sl;
+        const int s = base < n ? __ldg(srp + base) : 0;
+        const int a = s & ~3;
+        int e = 0;
+        bool in = false;
+        if (base + t < n) {
+            e = __ldg(srp + base + t + 1);
+            in = e - a <= cap;
+            rpw[t + 1] = e;
+        }
+        int rows = __syncthreads_count(in);  // the predicate is monotone in t: a prefix
+        if (base < n && rows == 0) rows = 1;  // one row longer than the buffer: read it from global
+        const int end = min(base + rows, n);
+        const int ee = base < n ? __ldg(srp + end) : 0;
+        const bool global = ee - a > cap;
+        if (t == 0) {
+            rpw[0] = s;
+            m[0] = base, m[1] = end, m[2] = a, m[3] = global;
+        }
+        if (base < n && !global) {
+            int* dst = buf + sl * cap;
+            const int v1 = ee >> 2;  // whole int4s [a/4, v1), then the tail ints
+            for (int v = (a >> 2) + t; v < v1; v += kChunk) {
+                const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + (v * 4 - a)));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(sci + v * 4));
+            }
+            for (int x = max(v1 * 4, a) + t; x < ee; x += kChunk) cp_async4(dst + (x - a), sci + x);
+        }
+        cp_commit();
+    };
+
+    stage(0, 0);
+    for (int k = 0;; ++k) {
+        const int sl = k & 1;
+        __syncthreads();
+        const int base = meta[4 * sl], end = meta[4 * sl + 1], a = meta[4 * sl + 2];
+        if (base >= n) break;
+        stage(end, sl ^ 1);  // prefetch the next chunk while this one is processed
+        asm volatile("cp.async.wait_group 1;" ::);
+        __syncthreads();
+        const int* rpw = rpb + sl * (kChunk + 4);
+        const int* cols = meta[4 * sl + 3] ? sci + a : buf + sl * cap;  // column q at cols[q - a]
+        const int rows = end - base;
+        // phase A: short rows one per thread; long rows one per warp, lanes across the columns
+        if (kLane) {
+            if (t < rows) {
+                const int i = base + t;
+                bool cov = (bits[i >> 5] >> (i & 31)) & 1u;
+                for (int q = rpw[t]; q < rpw[t + 1] && !cov; ++q) {
+                    const int j = cols[q - a];
+                    cov = (bits[j >> 5] >> (j & 31)) & 1u;
+                }
+                cflag[t] = !cov;
+            }
+        } else
+        for (int r = w; r < rows; r += 32) {
+            const int i = base + r;
+            bool cov = (bits[i >> 5] >> (i & 31)) & 1u;
+            if (!cov) {
+                bool hit = false;
+                for (int q = rpw[r] + lane; q < rpw[r + 1]; q += 32) {
+                    const int j = cols[q - a];
+                    hit |= (bits[j >> 5] >> (j & 31)) & 1u;
+                }
+                cov = __any_sync(kFull, hit);
+            }
+            if (lane == 0) cflag[r] = !cov;
+        }
+        __syncthreads();
+        // phase B: candidates in index order
+        if (kLane && w == 0) {
+            // lane-parallel rounds over 32 rows: every undecided candidate re-tests its own row; the
+            // lowest still-uncovered one is a seed (everything below it is decided), the covered
+            // ones are final; repeat until the group is decided
+            for (int g = 0; g < rows; g += 32) {
+                const int r = g + lane, i = base + r;
+                bool und = r < rows && cflag[r];
+                const int q0 = r < rows ? rpw[r] : 0, q1 = r < rows ? rpw[r + 1] : 0;
+                for (;;) {
+                    bool cov = false;
+                    if (und) {
+                        cov = (bits[i >> 5] >> (i & 31)) & 1u;
+                        for (int q = q0; q < q1 && !cov; ++q) {
+                            const int j = cols[q - a];
+                            cov = (bits[j >> 5] >> (j & 31)) & 1u;
+                        }
+                    }
+                    und = und && !cov;
+                    const unsigned U = __ballot_sync(kFull, und);
+                    if (!U) break;
+                    const int leader = __ffs(U) - 1;
+                    const int s0 = __shfl_sync(kFull, q0, leader), s1 = __shfl_sync(kFull, q1, leader);
+                    if (lane == leader) {
+                        atomicOr(bits + (i >> 5), 1u << (i & 31));
+                        status[i] = SEED;
+                        und = false;
+                    }
+                    for (int q = s0 + lane; q < s1; q += 32) {
+                        const int j = cols[q - a];
+                        atomicOr(bits + (j >> 5), 1u << (j & 31));
+                    }
+                    __syncwarp();
+                }
+            }
+        } else if (w == 0) {
+            bool seeded = false;
+            for (int g = 0; g < rows; g += 32) {
+                unsigned m = __ballot_sync(kFull, g + lane < rows && cflag[g + lane]);
+                while (m) {
+                    const int r = g + __ffs(m) - 1;
+                    m &= m - 1;
+                    const int i = base + r, q0 = rpw[r], q1 = rpw[r + 1];
+                    bool cov = false;
+                    if (seeded) {
+                        bool hit = lane == 0 && ((bits[i >> 5] >> (i & 31)) & 1u);
+                        for (int q = q0 + lane; q < q1; q += 32) {
+                            const int j = cols[q - a];
+                            hit |= (bits[j >> 5] >> (j & 31)) & 1u;
+                        }
+                        cov = __any_sync(kFull, hit);
+                    }
+                    if (!cov) {  // seed: assign N[i]
+                        if (lane == 0) {
+                            atomicOr(bits + (i >> 5), 1u << (i & 31));
+                            status[i] = SEED;
+                        }
+                        for (int q = q0 + lane; q < q1; q += 32) {
+                            const int j = cols[q - a];
+                            atomicOr(bits + (j >> 5), 1u << (j & 31));
+                        }
+                        seeded = true;
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::);
+}
+
+// shared memory of k_greedy_chunk for n rows and a column buffer of cap ints per slot
+inline size_t chunk_smem(int n, int cap) {
+    const size_t words = (size_t)(((n + 31) / 32 + 3) & ~3);
+    return sizeof(int) * (words + 2 * (kChunk + 4) + kChunk + 8 + 2 * (size_t)cap);
 }
 
 __global__ void k_seed_flags(int n, const int* __restrict__ status, int* __restrict__ flag) {
@@ -488,7 +661,28 @@ int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& 
     DBuf<unsigned> ticket(c, 1);
     CK(cudaMemsetAsync(status.p, 0, sizeof(int) * (size_t)n_core, c->stream));
     CK(cudaMemsetAsync(ticket.p, 0, sizeof(unsigned), c->stream));
-    if (n_core <= kSeqMax && !std::getenv("IBMGPU_NO_SEQ_AGG")) {
+    // IBMGPU_AGG=seq|chunk|lfmis forces a pass-1 kernel (A/B timing, tests); all give the same seeds
+    const char* force = std::getenv("IBMGPU_AGG");
+    const std::string pick = force ? force : "";
+    int max_smem = 0;
+    CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+    const size_t fixed = chunk_smem(n_core, 0);
+    const int cap = fixed < (size_t)max_smem ? (int)(((size_t)max_smem - fixed) / 8) & ~3 : 0;
+    // Default: the chunked loop (one row per thread/lane) up to kChunkMax rows, the LFMIS above.
+    // Measured (ms, chunked-lane vs LFMIS): flapping L2 66k rows 5.6 vs 19.0, L3 6.3k 0.49 vs 4.5;
+    // S-4M L3 78k 7.9 vs 16.6, L2 351k 42.9 vs 19.6; flapping L1 199k 32 vs 3.7 (the single CTA's
+    // serial rounds grow with the seed count; the LFMIS spreads over all SMs).
+    constexpr int kChunkMax = 131072;
+    const bool chunk_ok = cap >= 4096;
+    const bool lane = pick != "chunkw";
+    const bool use_chunk = pick.rfind("chunk", 0) == 0 ? chunk_ok : pick.empty() ? chunk_ok && n_core <= kChunkMax : false;
+    if (use_chunk) {
+        const size_t smem = chunk_smem(n_core, cap);
+        auto kern = lane ? k_greedy_chunk<true> : k_greedy_chunk<false>;
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<1, kChunk, smem, c->stream>>>(n_core, S.rp.p, S.ci.p, status.p, cap);
+        CK_LAUNCH(c);
+    } else if (pick == "seq") {
         const size_t smem = sizeof(unsigned) * (size_t)((n_core + 31) / 32) + sizeof(int) * (kGD * kGW + kWin + kGD + 1);
         CK(cudaFuncSetAttribute(k_greedy_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_greedy_seq<<<1, 32, smem, c->stream>>>(n_core, S.rp.p, S.ci.p, status.p);

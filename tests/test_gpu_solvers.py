@@ -108,9 +108,23 @@ def test_sa_hierarchy_bitwise_small_case(port):
         assert np.array_equal(agg[:n_core], d[f"L{l}_agg"])
 
 
+def _agg_dev(A, theta, n_core):
+    import ctypes as C
+    agg = np.zeros(max(n_core, 1), np.int32)
+    Ad = dev(A)
+    n = C.c_int()
+    Ad.ctx.check(Ad.ctx.lib.ibmgpu_aggregate(Ad.ctx.h, Ad.h, theta, n_core,
+                                             agg.ctypes.data_as(C.POINTER(C.c_int)), C.byref(n)))
+    return n.value, agg[:n_core]
+
+
+@pytest.mark.parametrize("kernel", ["", "seq", "chunkl", "chunkw", "lfmis"])
 @pytest.mark.parametrize("name", ["cavity", "cylinder_re40_smoke", "flapping_smoke", "cylinder_re40"])
-def test_aggregation_matches_golden(ref, name):
-    """Device greedy aggregation == sa_detail::aggregate on every level of the reference hierarchy."""
+def test_aggregation_matches_golden(ref, name, kernel, monkeypatch):
+    """Device greedy aggregation == sa_detail::aggregate on every level of the reference hierarchy,
+    with the default pass-1 kernel choice and with each pass-1 kernel forced (IBMGPU_AGG)."""
+    if kernel:
+        monkeypatch.setenv("IBMGPU_AGG", kernel)
     gold = H.hashes()[name]
     c = ref.case(H.case(name))
     h = c.hierarchy()
@@ -125,6 +139,34 @@ def test_aggregation_matches_golden(ref, name):
                                                  agg.ctypes.data_as(C.POINTER(C.c_int)), C.byref(n)))
         assert n.value == gl["n_agg"]
         assert hashlib.sha256(np.ascontiguousarray(agg[:n_core], np.int32).tobytes()).hexdigest() == gl["agg"]
+
+
+@pytest.mark.parametrize("kernel", ["seq", "chunkl", "chunkw", "lfmis"])
+@pytest.mark.parametrize("n,deg,seed", [(1, 0, 0), (37, 3, 1), (5000, 40, 2), (40000, 24, 3), (3000, 900, 4)])
+def test_aggregation_kernels_random_graphs(port, monkeypatch, kernel, n, deg, seed):
+    """Each pass-1 kernel == the oracle's sequential greedy (amg.hpp:79-107) on random symmetric
+    graphs: banded-plus-random pattern, isolated rows, rows longer than a chunk's staging buffer."""
+    monkeypatch.setenv("IBMGPU_AGG", kernel)
+    rng = np.random.default_rng(seed)
+    k = rng.integers(0, deg + 1, n) if deg else np.zeros(n, np.int64)
+    k[np.arange(n) % 97 == 5] = 0  # isolated rows
+    src = np.repeat(np.arange(n), k)
+    near = src + rng.integers(-deg, deg + 1, len(src))
+    far = rng.integers(0, n, len(src))
+    dst = np.clip(np.where(rng.random(len(src)) < 0.5, near, far), 0, n - 1)
+    if seed == 3:  # a hub row longer than the staging buffer (read from global memory)
+        src = np.concatenate([src, np.full(n, 7)])
+        dst = np.concatenate([dst, np.arange(n)])
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    rr = np.concatenate([src, dst, np.arange(n)])
+    cc = np.concatenate([dst, src, np.arange(n)])
+    vv = np.concatenate([-np.ones(2 * len(src)), np.full(n, 4.0 * deg + 4.0)])
+    A = port.from_triplets(n, n, rr, cc, vv)
+    n_ref, agg_ref = port.aggregate(A, 1e-9, n)
+    n_dev, agg_dev = _agg_dev(A, 1e-9, n)
+    assert n_dev == n_ref
+    assert np.array_equal(agg_dev, np.asarray(agg_ref, np.int32)[:n])
 
 
 def test_vcycle_matches_oracle_and_is_self_adjoint():
