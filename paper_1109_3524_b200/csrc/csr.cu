@@ -304,8 +304,11 @@ void mat_plan(Ctx* c, Mat* m) {
         if (few_long && ns > 0 && enough_rows) {
             // SELL-32-sigma: sort short rows by length within 512-slot windows; accept if padding <= 25%
             std::vector<int> perm(shortrows);
-            for (int w0 = 0; w0 < ns; w0 += kSigma) {
-                const int w1 = std::min(ns, w0 + kSigma);
+            // windows are independent: sort them on all host threads (same result as serial)
+            const int n_win = (ns + kSigma - 1) / kSigma;
+#pragma omp parallel for schedule(static) if (n_win >= 64)
+            for (int wi = 0; wi < n_win; ++wi) {
+                const int w0 = wi * kSigma, w1 = std::min(ns, w0 + kSigma);
                 std::stable_sort(perm.begin() + w0, perm.begin() + w1,
                                  [&](int a, int b) { return rp[a + 1] - rp[a] > rp[b + 1] - rp[b]; });
             }
