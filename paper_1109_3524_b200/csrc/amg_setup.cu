@@ -201,6 +201,22 @@ __global__ void __launch_bounds__(32) k_greedy_seq(int n, const int* __restrict_
 // settled in phase A.
 constexpr int kChunk = 1024;
 
+// any assigned node among cols[q0, q1): four independent column loads in flight per step
+__device__ __forceinline__ bool any_assigned(const unsigned* bits, const int* cols, int q0, int q1) {
+    int q = q0;
+    for (; q + 4 <= q1; q += 4) {
+        const int j0 = cols[q], j1 = cols[q + 1], j2 = cols[q + 2], j3 = cols[q + 3];
+        const unsigned b = (bits[j0 >> 5] >> (j0 & 31)) | (bits[j1 >> 5] >> (j1 & 31)) |
+                           (bits[j2 >> 5] >> (j2 & 31)) | (bits[j3 >> 5] >> (j3 & 31));
+        if (b & 1u) return true;
+    }
+    for (; q < q1; ++q) {
+        const int j = cols[q];
+        if ((bits[j >> 5] >> (j & 31)) & 1u) return true;
+    }
+    return false;
+}
+
 template <bool kLane>
 __global__ void __launch_bounds__(kChunk) k_greedy_chunk(int n, const int* __restrict__ srp,
                                                          const int* __restrict__ sci, int* __restrict__ status,
@@ -265,11 +281,7 @@ __global__ void __launch_bounds__(kChunk) k_greedy_chunk(int n, const int* __res
         if (kLane) {
             if (t < rows) {
                 const int i = base + t;
-                bool cov = (bits[i >> 5] >> (i & 31)) & 1u;
-                for (int q = rpw[t]; q < rpw[t + 1] && !cov; ++q) {
-                    const int j = cols[q - a];
-                    cov = (bits[j >> 5] >> (j & 31)) & 1u;
-                }
+                const bool cov = ((bits[i >> 5] >> (i & 31)) & 1u) || any_assigned(bits, cols - a, rpw[t], rpw[t + 1]);
                 cflag[t] = !cov;
             }
         } else
@@ -298,13 +310,7 @@ __global__ void __launch_bounds__(kChunk) k_greedy_chunk(int n, const int* __res
                 const int q0 = r < rows ? rpw[r] : 0, q1 = r < rows ? rpw[r + 1] : 0;
                 for (;;) {
                     bool cov = false;
-                    if (und) {
-                        cov = (bits[i >> 5] >> (i & 31)) & 1u;
-                        for (int q = q0; q < q1 && !cov; ++q) {
-                            const int j = cols[q - a];
-                            cov = (bits[j >> 5] >> (j & 31)) & 1u;
-                        }
-                    }
+                    if (und) cov = ((bits[i >> 5] >> (i & 31)) & 1u) || any_assigned(bits, cols - a, q0, q1);
                     und = und && !cov;
                     const unsigned U = __ballot_sync(kFull, und);
                     if (!U) break;
