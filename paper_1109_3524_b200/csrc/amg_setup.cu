@@ -667,7 +667,7 @@ int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& 
     DBuf<unsigned> ticket(c, 1);
     CK(cudaMemsetAsync(status.p, 0, sizeof(int) * (size_t)n_core, c->stream));
     CK(cudaMemsetAsync(ticket.p, 0, sizeof(unsigned), c->stream));
-    // IBMGPU_AGG=seq|chunk|lfmis forces a pass-1 kernel (A/B timing, tests); all give the same seeds
+    // IBMGPU_AGG=seq|chunkl|chunkw|lfmis forces a pass-1 kernel (A/B timing, tests); all give the same seeds
     const char* force = std::getenv("IBMGPU_AGG");
     const std::string pick = force ? force : "";
     int max_smem = 0;
