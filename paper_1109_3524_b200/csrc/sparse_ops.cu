@@ -472,6 +472,13 @@ struct HashChunk {
     double a[32];
 };
 
+// next row for this warp from a global counter (lane 0 takes it, the warp shares it)
+__device__ __forceinline__ int next_row(unsigned* next, int lane) {
+    unsigned r = 0;
+    if (lane == 0) r = atomicAdd(next, 1u);
+    return static_cast<int>(__shfl_sync(kFull, r, 0));
+}
+
 __device__ __forceinline__ int chunk_load(HashChunk& ch, int c0, int e, const int* __restrict__ aci,
                                           const double* __restrict__ av, const int* __restrict__ brp, int lane,
                                           bool values) {
@@ -516,14 +523,16 @@ __global__ void __launch_bounds__(kSymWarps * 32) k_hash_symbolic(int r0, int ro
                                                                   const int* __restrict__ bci, int* __restrict__ cnt,
                                                                   int* __restrict__ maxcnt,
                                                                   const long long* __restrict__ rprod,
-                                                                  long long limit) {
+                                                                  long long limit, unsigned* __restrict__ next) {
     extern __shared__ int hsm[];
     __shared__ HashChunk chunks[kSymWarps];
     __shared__ int counter[kSymWarps];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int* keys = hsm + w * kHashSym;
     HashChunk& ch = chunks[w];
-    for (int row = blockIdx.x * kSymWarps + w; row < rows; row += gridDim.x * kSymWarps) {
+    for (;;) {
+        const int row = next_row(next, lane);  // rows handed out one at a time: no CTA-wave tail
+        if (row >= rows) break;
         if (rprod[row] > limit) continue;  // long row: counted by the ESC pass
         for (int t = lane; t < kHashSym; t += 32) keys[t] = -1;
         if (lane == 0) counter[w] = 0;
@@ -565,7 +574,8 @@ __global__ void k_hash_numeric(int r0, int rows, const int* __restrict__ arp, co
                                const double* __restrict__ av, const int* __restrict__ brp,
                                const int* __restrict__ bci, const double* __restrict__ bv,
                                const int* __restrict__ crp, int* __restrict__ cci, double* __restrict__ cv,
-                               int slots, const long long* __restrict__ rprod, long long limit) {
+                               int slots, const long long* __restrict__ rprod, long long limit,
+                               unsigned* __restrict__ next) {
     extern __shared__ double hsd[];
     const int nw = blockDim.x >> 5;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -575,7 +585,9 @@ __global__ void k_hash_numeric(int r0, int rows, const int* __restrict__ arp, co
     double* prod = reinterpret_cast<double*>(chunks + nw) + w * 32;
     HashChunk& ch = chunks[w];
     const int mask = slots - 1;
-    for (int row = blockIdx.x * nw + w; row < rows; row += gridDim.x * nw) {
+    for (;;) {
+        const int row = next_row(next, lane);
+        if (row >= rows) break;
         if (rprod[row] > limit) continue;
         for (int t = lane; t < slots; t += 32) {
             keys[t] = -1;
@@ -753,9 +765,13 @@ Mat* spmm_hash(Ctx* c, const Mat* A, int r0, int r1, const Mat* B, const long lo
     std::unique_ptr<Mat> hold(Cl);
     const size_t sym_smem = sizeof(int) * (size_t)kSymWarps * kHashSym;
     CK(cudaFuncSetAttribute(k_hash_symbolic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem));
-    const int sgrid = std::min((rows + kSymWarps - 1) / kSymWarps, c->num_sms * 4);
+    int sym_occ = 0;  // persistent grid: every CTA resident, rows handed out dynamically
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sym_occ, k_hash_symbolic, kSymWarps * 32, sym_smem));
+    const int sgrid = std::min((rows + kSymWarps - 1) / kSymWarps, c->num_sms * std::max(sym_occ, 1));
+    DBuf<unsigned> next(c, 2);
+    CK(cudaMemsetAsync(next.p, 0, 2 * sizeof(unsigned), c->stream));
     k_hash_symbolic<<<sgrid, kSymWarps * 32, sym_smem, c->stream>>>(r0, rows, A->rp.p, A->ci.p, B->rp.p, B->ci.p,
-                                                                      cnt.p, mx.p, rprod, limit);
+                                                                      cnt.p, mx.p, rprod, limit, next.p);
     CK_LAUNCH(c);
     const int maxc = d2h_scalar(c, mx.p);
     lap("symbolic", maxc);
@@ -771,9 +787,11 @@ Mat* spmm_hash(Ctx* c, const Mat* A, int r0, int r1, const Mat* B, const long lo
     m->ci.alloc(c, (size_t)std::max(m->nnz, 1));
     m->v.alloc(c, (size_t)std::max(m->nnz, 1));
     CK(cudaFuncSetAttribute(k_hash_numeric, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int ngrid = std::min((rows + nw - 1) / nw, c->num_sms * 8);
+    int num_occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&num_occ, k_hash_numeric, nw * 32, smem));
+    const int ngrid = std::min((rows + nw - 1) / nw, c->num_sms * std::max(num_occ, 1));
     k_hash_numeric<<<ngrid, nw * 32, smem, c->stream>>>(r0, rows, A->rp.p, A->ci.p, A->v.p, B->rp.p, B->ci.p, B->v.p,
-                                                        m->rp.p, m->ci.p, m->v.p, slots, rprod, limit);
+                                                        m->rp.p, m->ci.p, m->v.p, slots, rprod, limit, next.p + 1);
     CK_LAUNCH(c);
     if (nl > 0) {
         k_place_rows<<<nl, 256, 0, c->stream>>>(nl, lidx.p, Cl->rp.p, Cl->ci.p, Cl->v.p, m->rp.p, m->ci.p, m->v.p);
