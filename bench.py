@@ -10,7 +10,8 @@ A "step" is one Stepper::advance (stepper.hpp:231-356): explicit terms, PCG-diag
 SA-PCG coupled solve, projection and invariants, all resident in HBM (device-built operators and
 SA hierarchy). Prints ONE JSON line (rank 0). Default workload: C2 = impulsively started cylinder,
 Re 40, ~1M cells (cylinder_re40.cfg at h_min 0.002 -> 1042^2), BASELINE.json configs[1]; the
-S-4M (configs[2]) per-iteration roofline is reported alongside under "s4m" unless --no-s4m.
+S-4M (configs[2]) per-iteration roofline is reported alongside under "s4m" unless --no-s4m, and
+the moving-body case (configs[3]) under "flapping" unless --no-flapping.
 
 --impl reference runs the reference's own CPU implementation (oracle/_ref/libibmref.so, the
 unmodified reference headers) on the same case with all host threads; it never touches the GPU.
@@ -277,9 +278,12 @@ def s4m_probe(args) -> dict:
     b_it2, hinfo = hier_bytes(st.hierarchy())
     st.advance()
     ms, its = [], []
+    step_ms = []
     for _ in range(max(2, min(args.steps, 5))):
         r = st.advance()
-        ms.append(st.phase_ms()["solve2"])
+        ph = st.phase_ms()
+        ms.append(ph["solve2"])
+        step_ms.append(sum(ph.values()))  # device-timed phases of the whole step
         its.append(r.solve2_iters)
     peak, kind = load_peaks()
     it_ms = sum(ms) / sum(its)
@@ -287,8 +291,30 @@ def s4m_probe(args) -> dict:
     return {"grid": [st.nx, st.ny], "n_lambda": st.n_lambda, "setup_s": round(setup, 2),
             "cg_iters_per_step": sum(its) / len(its), "cg_iteration_ms": round(it_ms, 4),
             "b_it2_gb": round(b_it2 / 1e9, 3), "achieved_gbs": round(ach, 1), "frac_measured": round(ach / peak, 4),
-            "frac_of_8tbs": round(ach / 8000, 4), "steps_per_s": round(1e3 / (sum(ms) / len(ms)), 3),
+            "frac_of_8tbs": round(ach / 8000, 4), "steps_per_s": round(1e3 / (sum(step_ms) / len(step_ms)), 3),
             "sa_levels": len(hinfo["levels"]), "n_c": hinfo["n_c"]}
+
+
+def flapping_probe(args) -> dict:
+    """Moving body (BASELINE configs[3]): E, H, Q, Q^T, lhs2 rebuilt every step and the SA hierarchy
+    every n_pc steps, all on the device. Wall clock around whole Stepper.advance calls."""
+    from paper_1109_3524_b200 import ibm
+    cfg, h_min, dt, _ = WORKLOADS["flapping"]
+    st = ibm.Stepper(os.path.join(CASES, cfg + ".cfg"), h_min=h_min, dt=dt)
+    for _ in range(3):
+        st.advance()
+    st.ctx.sync()
+    n = 10
+    t0 = time.perf_counter()
+    reps = [st.advance() for _ in range(n)]
+    st.ctx.sync()
+    wall = time.perf_counter() - t0
+    return {"case": cfg + ".cfg", "grid": [st.nx, st.ny], "n_lambda": st.n_lambda, "steps": n,
+            "steps_per_s": round(n / wall, 3),
+            "operator_rebuild_ms_per_step": round(1e3 * sum(r.t_assembly for r in reps) / n, 3),
+            "hierarchy_rebuild_ms_per_step": round(1e3 * sum(r.t_precond for r in reps) / n, 3),
+            "hierarchy_rebuilds": sum(r.rebuilt_hierarchy for r in reps),
+            "cg_iters_per_step": sum(r.solve2_iters for r in reps) / n}
 
 
 def cpu_baseline(args) -> dict:
@@ -354,6 +380,7 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-s4m", action="store_true")
+    ap.add_argument("--no-flapping", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the C5 grid-size sweep (1024^2..4096^2)")
     ap.add_argument("--parallel", default="slab", choices=["slab", "replicas"],
                     help="N>1: row-slab distributed solve 2 over NCCL (one simulation), or N replicas")
@@ -397,6 +424,11 @@ def main():
                 out["s4m"] = s4m_probe(args)
             except Exception as e:  # report, never hide
                 out["s4m"] = {"error": str(e)}
+        if not args.no_flapping and args.workload != "flapping" and world == 1:
+            try:
+                out["flapping"] = flapping_probe(args)
+            except Exception as e:
+                out["flapping"] = {"error": str(e)}
         if not args.no_sweep and world == 1 and args.workload == "c2":
             try:  # BASELINE metric "CG iters/sec vs grid size" (configs[4] synthetic grids)
                 sys.path.insert(0, os.path.join(ROOT, "tools"))
