@@ -308,9 +308,20 @@ __global__ void __launch_bounds__(kChunk) k_greedy_chunk(int n, const int* __res
                 const int r = g + lane, i = base + r;
                 bool und = r < rows && cflag[r];
                 const int q0 = r < rows ? rpw[r] : 0, q1 = r < rows ? rpw[r + 1] : 0;
+                // the first kReg columns of the row stay in registers for the repeated tests: each
+                // round is then kReg independent bitmap loads instead of a dependent column walk
+                constexpr int kReg = 16;
+                int rc[kReg];
+#pragma unroll
+                for (int u = 0; u < kReg; ++u) rc[u] = (und && q0 + u < q1) ? cols[q0 + u - a] : i;
                 for (;;) {
                     bool cov = false;
-                    if (und) cov = ((bits[i >> 5] >> (i & 31)) & 1u) || any_assigned(bits, cols - a, q0, q1);
+                    if (und) {
+                        unsigned b = bits[i >> 5] >> (i & 31);
+#pragma unroll
+                        for (int u = 0; u < kReg; ++u) b |= bits[rc[u] >> 5] >> (rc[u] & 31);
+                        cov = (b & 1u) || (q1 - q0 > kReg && any_assigned(bits, cols - a, q0 + kReg, q1));
+                    }
                     und = und && !cov;
                     const unsigned U = __ballot_sync(kFull, und);
                     if (!U) break;
