@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kChunk) k_greedy_chunk(int n, const int* __res
                 cflag[t] = !cov;
             }
         } else
-        for (int r = w; r < rows; r += 32) {
+        for (int r = w; r < rows; r += kChunk / 32) {
             const int i = base + r;
             bool cov = (bits[i >> 5] >> (i & 31)) & 1u;
             if (!cov) {
