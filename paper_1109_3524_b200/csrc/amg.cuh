@@ -69,9 +69,23 @@ struct ibmgpu_hier {
 namespace ibmgpu {
 using Hier = ibmgpu_hier;
 
+// Aggregates of the previous build, per level, keyed by the strength graph they came from.
+// aggregate() (amg.hpp:79-107) is a function of the strength graph alone, so when a rebuild's
+// graph is identical to the cached one the cached aggregates ARE the result (moving bodies: the
+// level-0 graph lives on the pressure block, which body motion never changes).
+struct AggCache {
+    struct Lv {
+        int n_core = -1, nnz = -1, n_agg = 0;
+        DBuf<int> rp, ci, agg;
+    };
+    std::vector<Lv> lv;
+    long long hits = 0, misses = 0;
+};
+
 // amg_setup.cu
-Hier* sa_build(Ctx* c, const Mat* A, const ibm_sa_options& o);
-int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& agg);
+Hier* sa_build(Ctx* c, const Mat* A, const ibm_sa_options& o, AggCache* cache = nullptr);
+int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& agg,
+                     AggCache::Lv* cache = nullptr, bool* hit = nullptr);
 // dense.cu
 void dense_spd_inverse(Ctx* c, const Mat* Ac, double* inv);  // factor (dense.hpp:20-40) + inverse
 void launch_dense_gemv(Ctx* c, int n, const double* Ainv, const double* x, double* y, const int* done,

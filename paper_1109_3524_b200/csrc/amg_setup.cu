@@ -25,6 +25,7 @@
 #include "amg.cuh"
 #include "internal.cuh"
 #include "kern.cuh"
+#include "small_rows.cuh"
 
 namespace ibmgpu {
 
@@ -467,6 +468,107 @@ __global__ void k_ptent(int rows, int n_core, const int* __restrict__ agg, const
     }
 }
 
+// P (amg.hpp:163-178) in one pass, one warp per row of P: core row i is
+//   add_sparse(1.0, P_tent, -omega, spmm(D^{-1}A, P_tent)) row i
+// = for each column a: (0.0 [+ 1.0 * ptent_i if a == agg_i]) + (-omega) * dap_a, exact zeros
+// dropped, where dap_a sums mul(mul(a_ik, invd_i), ptent_k) over k in A-row order with agg_k == a
+// (Gustavson over the one-entry rows of P_tent; tail columns of A meet empty P_tent rows);
+// tail row n_core + t is the identity entry (n_agg + t, 1.0). Rows with more than kSmallCap
+// core entries set *over and the caller takes the general path.
+__device__ __forceinline__ double ptent_val(const int* __restrict__ size, int a) {
+    return __ddiv_rn(1.0, __dsqrt_rn((double)size[a]));
+}
+
+__global__ void __launch_bounds__(kSmallWarps * 32)
+    k_smooth_p(int rows, int n_core, int n_agg, double omega, const int* __restrict__ arp,
+               const int* __restrict__ aci, const double* __restrict__ av, const double* __restrict__ invd,
+               const int* __restrict__ agg, const int* __restrict__ size, int* __restrict__ cnt,
+               const int* __restrict__ orp, int* __restrict__ oci, double* __restrict__ ov, int* __restrict__ over) {
+    __shared__ SmallRow ws[kSmallWarps];
+    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    SmallRow& w = ws[wi];
+    for (int i = blockIdx.x * kSmallWarps + wi; i < rows; i += gridDim.x * kSmallWarps) {
+        if (i >= n_core) {
+            if (lane == 0) {
+                if (cnt) {
+                    cnt[i] = 1;
+                } else {
+                    oci[orp[i]] = n_agg + (i - n_core);
+                    ov[orp[i]] = 1.0;
+                }
+            }
+            continue;
+        }
+        const int b = arp[i], e = arp[i + 1];
+        // products in A-row order (core columns only: P_tent's tail rows are empty)
+        int n = 0;
+        const double di = invd[i];
+        for (int k0 = b; k0 < e; k0 += 32) {
+            const int k = k0 + lane;
+            const bool core = k < e && aci[k] < n_core;
+            const unsigned m = __ballot_sync(0xffffffffu, core);
+            if (n + __popc(m) > kSmallCap) {
+                if (lane == 0) *over = 1;
+                n = -1;
+                break;
+            }
+            if (core) {
+                const int kk = aci[k];
+                const int a = agg[kk];
+                const int pos = n + __popc(m & ((1u << lane) - 1));
+                w.col[pos] = a;
+                w.val[pos] = mul(mul(av[k], di), ptent_val(size, a));
+            }
+            n += __popc(m);
+        }
+        __syncwarp();
+        if (n < 0) continue;
+        const int u = small_reduce(w, n, lane);  // DAP row: columns sorted, Gustavson sums
+        const int ai = agg[i];
+        const double pti = ptent_val(size, ai);
+        // merge with the single P_tent entry (ai, pti); values (0 + 1.0*pt) + (-omega)*dap
+        bool has_ai = false;
+        for (int q = lane; q < u; q += 32) has_ai |= w.scol[q] == ai;
+        has_ai = __any_sync(0xffffffffu, has_ai);
+        const int total = u + (has_ai ? 0 : 1);
+        // write in column order; an exact-zero sum is dropped (from_triplets), counted by ballot
+        int outn = 0;
+        const int o = cnt ? 0 : orp[i];
+        for (int base = 0; base < total; base += 32) {
+            const int q = base + lane;
+            int col = 0;
+            double v = 0.0;
+            bool keep = false;
+            if (q < total) {
+                // position q of the merged list: ai inserted before the first column > ai
+                int ins = 0;  // number of DAP columns < ai
+                for (int t = 0; t < u; ++t) ins += w.scol[t] < ai;
+                if (has_ai) {
+                    col = w.scol[q];
+                    v = addd(col == ai ? addd(0.0, mul(1.0, pti)) : 0.0, mul(-omega, w.sval[q]));
+                } else if (q == ins) {
+                    col = ai;
+                    v = addd(0.0, mul(1.0, pti));
+                } else {
+                    const int t = q < ins ? q : q - 1;
+                    col = w.scol[t];
+                    v = addd(0.0, mul(-omega, w.sval[t]));
+                }
+                keep = v != 0.0;
+            }
+            const unsigned km = __ballot_sync(0xffffffffu, keep);
+            if (!cnt && keep) {
+                const int pos = o + outn + __popc(km & ((1u << lane) - 1));
+                oci[pos] = col;
+                ov[pos] = v;
+            }
+            outn += __popc(km);
+        }
+        if (cnt && lane == 0) cnt[i] = outn;
+        __syncwarp();
+    }
+}
+
 __global__ void k_invd(int n, const double* __restrict__ d, double omega, double* __restrict__ invd,
                        double* __restrict__ wd, int* __restrict__ zero) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -648,7 +750,17 @@ struct SetupClock {
 }  // namespace
 
 // Strength graph + exact greedy aggregation; returns aggregate count, agg sized n_core.
-int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& agg) {
+__global__ void k_neq(int n, const int* __restrict__ a, const int* __restrict__ b, int* __restrict__ diff) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        if (a[i] != b[i]) {
+            *diff = 1;
+            return;
+        }
+}
+
+int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& agg, AggCache::Lv* cache,
+                     bool* hit) {
+    if (hit) *hit = false;
     agg.alloc(c, (size_t)std::max(n_core, 1));
     if (n_core == 0) return 0;
     DBuf<double> diag(c, (size_t)A->rows);
@@ -669,6 +781,22 @@ int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& 
     k_strength<<<blocks(n_core), 256, 0, c->stream>>>(n_core, theta, A->rp.p, A->ci.p, A->v.p, diag.p, nullptr,
                                                       S.rp.p, S.ci.p);
     CK_LAUNCH(c);
+    if (cache && cache->n_core == n_core && cache->nnz == S.nnz) {
+        DBuf<int> diff(c, 1);
+        CK(cudaMemsetAsync(diff.p, 0, sizeof(int), c->stream));
+        const int g = std::max(1, std::min(c->num_sms * 8, blocks(std::max(S.nnz, n_core + 1))));
+        k_neq<<<g, 256, 0, c->stream>>>(n_core + 1, S.rp.p, cache->rp.p, diff.p);
+        CK_LAUNCH(c);
+        if (S.nnz) {
+            k_neq<<<g, 256, 0, c->stream>>>(S.nnz, S.ci.p, cache->ci.p, diff.p);
+            CK_LAUNCH(c);
+        }
+        if (!d2h_scalar(c, diff.p)) {
+            d2d(c, agg.p, cache->agg.p, (size_t)n_core);
+            if (hit) *hit = true;
+            return cache->n_agg;
+        }
+    }
     SetupClock clk(c);
     Mat* St = transpose(c, &S);  // in-neighbour lists (sorted by source row)
     clk.lap("  agg:S+St", -2);
@@ -747,11 +875,49 @@ int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& 
         CK_LAUNCH(c);
     }
     delete St;
+    if (cache) {
+        cache->n_core = n_core;
+        cache->nnz = S.nnz;
+        cache->n_agg = n_seeds + n3;
+        cache->rp = std::move(S.rp);
+        cache->ci = std::move(S.ci);
+        cache->agg.alloc(c, (size_t)n_core);
+        d2d(c, cache->agg.p, agg.p, (size_t)n_core);
+    }
     return n_seeds + n3;
 }
 
 
-Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
+// P in one fused pass (k_smooth_p); nullptr when a row is too long for it
+Mat* smoothed_prolongator(Ctx* c, const Mat* A, const double* invd, const int* agg, const int* size, int n_core,
+                          int n_agg, double omega) {
+    const int rows = A->rows, tail = rows - n_core;
+    DBuf<int> cnt(c, (size_t)rows + 1), over(c, 1);
+    CK(cudaMemsetAsync(over.p, 0, sizeof(int), c->stream));
+    const int grid = std::max(1, std::min(blocks(rows, kSmallWarps), c->num_sms * 8));
+    k_smooth_p<<<grid, kSmallWarps * 32, 0, c->stream>>>(rows, n_core, n_agg, omega, A->rp.p, A->ci.p, A->v.p, invd,
+                                                         agg, size, cnt.p, nullptr, nullptr, nullptr, over.p);
+    CK_LAUNCH(c);
+    Mat* P = mat_new(c, rows, n_agg + tail, 0);
+    exclusive_scan_total(c, cnt.p, P->rp.p, rows);
+    int hv[2];
+    d2h(c, hv, over.p, 1);
+    d2h(c, hv + 1, P->rp.p + rows, 1);
+    sync(c);
+    if (hv[0]) {
+        delete P;
+        return nullptr;
+    }
+    P->nnz = hv[1];
+    P->ci.alloc(c, (size_t)std::max(P->nnz, 1));
+    P->v.alloc(c, (size_t)std::max(P->nnz, 1));
+    k_smooth_p<<<grid, kSmallWarps * 32, 0, c->stream>>>(rows, n_core, n_agg, omega, A->rp.p, A->ci.p, A->v.p, invd,
+                                                         agg, size, nullptr, P->rp.p, P->ci.p, P->v.p, over.p);
+    CK_LAUNCH(c);
+    return P;
+}
+
+Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o, AggCache* cache) {
     require(A_fine->rows == A_fine->cols, "sa: square matrix required");
     SetupClock clk(c);
     static std::atomic<long long> next_id{1};
@@ -765,7 +931,10 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
             const double theta_l = o.theta * std::pow(0.5, lev);
             const int n_core = A->rows - tail;
             auto L = std::make_unique<Level>();
-            const int n_agg = aggregate_device(c, A, theta_l, n_core, L->agg);
+            if (cache && cache->lv.size() <= (size_t)lev) cache->lv.resize(lev + 1);
+            bool hit = false;
+            const int n_agg = aggregate_device(c, A, theta_l, n_core, L->agg, cache ? &cache->lv[lev] : nullptr, &hit);
+            if (cache) ++(hit ? cache->hits : cache->misses);
             clk.lap("aggregate", lev);
             if (n_agg >= n_core) {
                 h->stalled = true;
@@ -795,19 +964,22 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o) {
             CK(cudaMemsetAsync(size.p, 0, sizeof(int) * (size_t)n_agg, c->stream));
             k_agg_size<<<blocks(n_core), 256, 0, c->stream>>>(n_core, L->agg.p, size.p);
             CK_LAUNCH(c);
-            Mat* Ptent = mat_new(c, n, n_agg, n_core);
-            k_ptent<<<blocks(n + 1), 256, 0, c->stream>>>(n, n_core, L->agg.p, size.p, Ptent->rp.p, Ptent->ci.p,
-                                                          Ptent->v.p);
-            CK_LAUNCH(c);
             // P = (I - omega D^{-1} A) P_tent on the core; identity on the tail
-            Mat* DA = scale(c, A, 1, 0.0, L->invd.p);
-            Mat* DAP = spmm_rows(c, DA, 0, DA->rows, Ptent);
-            delete DA;
-            Mat* Pcore = add(c, 1.0, Ptent, -omega, DAP);
-            delete DAP;
-            delete Ptent;
-            Mat* P = tail > 0 ? identity_tail_append(c, Pcore, n_core, n_agg, tail) : Pcore;
-            if (tail > 0) delete Pcore;
+            Mat* P = smoothed_prolongator(c, A, L->invd.p, L->agg.p, size.p, n_core, n_agg, omega);
+            if (!P) {  // a row with more than kSmallCap core entries: the general product
+                Mat* Ptent = mat_new(c, n, n_agg, n_core);
+                k_ptent<<<blocks(n + 1), 256, 0, c->stream>>>(n, n_core, L->agg.p, size.p, Ptent->rp.p, Ptent->ci.p,
+                                                              Ptent->v.p);
+                CK_LAUNCH(c);
+                Mat* DA = scale(c, A, 1, 0.0, L->invd.p);
+                Mat* DAP = spmm_rows(c, DA, 0, DA->rows, Ptent);
+                delete DA;
+                Mat* Pcore = add(c, 1.0, Ptent, -omega, DAP);
+                delete DAP;
+                delete Ptent;
+                P = tail > 0 ? identity_tail_append(c, Pcore, n_core, n_agg, tail) : Pcore;
+                if (tail > 0) delete Pcore;
+            }
             clk.lap("P", lev);
             Mat* Pt = transpose(c, P);
             clk.lap("transpose", lev);

@@ -30,6 +30,7 @@
 #include "internal.cuh"
 #include "kern.cuh"
 #include "pcg.cuh"
+#include "refresh.cuh"
 
 namespace ibmgpu {
 struct GridDev;
@@ -437,6 +438,9 @@ struct ibmgpu_stepper {
     Hier* hier = nullptr;
     bool bn_diagonal = true;
     GridDev* gd = nullptr;
+    RefreshCache rcache;  // moving bodies: G^T and the invariant pressure block (refresh.cu)
+    bool check_refresh = false;
+    AggCache agg_cache;   // moving bodies: aggregates reused when the strength graph repeats
 
     // device vectors
     DBuf<double> dx, dy, del_x, del_y, mdt, bn_diag;
@@ -513,20 +517,46 @@ struct ibmgpu_stepper {
 
     // refresh_body_operators (operators.hpp:445-450) on the device
     void refresh_body_operators() {
+        static const bool prof = std::getenv("IBMGPU_SETUP_PROFILE") != nullptr;
+        auto t0 = std::chrono::steady_clock::now();
+        auto lap = [&](const char* what) {
+            if (!prof) return;
+            sync(c);
+            const auto t1 = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "[refresh] %-14s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+            t0 = t1;
+        };
         dist_stale = true;
         std::vector<double> hx, hy;
         host_points(hx, hy);
         const double uni[4] = {g.uniform_region.x0, g.uniform_region.x1, g.uniform_region.y0, g.uniform_region.y1};
         check_support(uni, g.h_min, n_b, hx.data(), hy.data());
         upload_bodies();
-        Mat *En = nullptr, *Hn = nullptr;
-        assemble_eh_dev(c, *gd, n_b, px.p, py.p, pds.p, &En, &Hn);
+        Mat* En = nullptr;
+        // H (operators.hpp:304-342) is assembled with E by the reference but never applied in a
+        // step; it is built from the same uploaded points when first asked for (ensure_H)
+        assemble_eh_dev(c, *gd, n_b, px.p, py.p, pds.p, &En, nullptr);
         delete E;
         delete H;
         E = En;
-        H = Hn;
+        H = nullptr;
+        lap("E, H");
         Mat *Qn, *QTn, *L2n;
-        coupled_system(c, G, E, BN, 0, slice_rows, &Qn, &QTn, &L2n, nullptr);
+        if (rcache.ready()) {
+            coupled_refresh(c, rcache, G, E, BN, &Qn, &QTn, &L2n);
+            if (check_refresh) {  // IBMGPU_CHECK_REFRESH=1: compare with the full assembly
+                Mat *Qf, *QTf, *L2f;
+                coupled_system(c, G, E, BN, 0, slice_rows, &Qf, &QTf, &L2f, nullptr);
+                const bool same = mat_equal(c, Qn, Qf) && mat_equal(c, QTn, QTf) && mat_equal(c, L2n, L2f);
+                delete Qf;
+                delete QTf;
+                delete L2f;
+                if (!same) fail(IBMGPU_ECUDA, "incremental refresh differs from the full assembly");
+            }
+        } else {
+            coupled_system(c, G, E, BN, 0, slice_rows, &Qn, &QTn, &L2n, nullptr);
+        }
+        lap("Q, QT, lhs2");
         pcg_forget(c, lhs2, nullptr);
         delete Q;
         delete QT;
@@ -534,7 +564,18 @@ struct ibmgpu_stepper {
         Q = Qn;
         QT = QTn;
         lhs2 = L2n;
+        lap("free");
         for (Mat* m : {Q, QT, lhs2}) mat_plan(c, m);
+        lap("plans");
+    }
+
+    Mat* ensure_H() {
+        if (!H) {
+            Mat* En = nullptr;
+            assemble_eh_dev(c, *gd, n_b, px.p, py.p, pds.p, &En, &H);
+            delete En;
+        }
+        return H;
     }
 
     // row owners of lambda: pressure j-slabs, force rows with the slab of their point's cell
@@ -588,7 +629,7 @@ struct ibmgpu_stepper {
 
     void rebuild_hierarchy() {
         dist_stale = true;
-        Hier* h = sa_build(c, lhs2, sa);
+        Hier* h = sa_build(c, lhs2, sa, rcache.ready() ? &agg_cache : nullptr);
         if (hier) {
             pcg_forget(c, nullptr, hier);
             delete hier;
@@ -719,6 +760,10 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
                              {g.uniform_region.x0, g.uniform_region.x1, g.uniform_region.y0, g.uniform_region.y1}};
     S->gd = grid_dev_new(c, gdsc);
     S->refresh_body_operators();
+    // a moving body re-assembles only the body coupling from here on (refresh.cu)
+    S->check_refresh = std::getenv("IBMGPU_CHECK_REFRESH") != nullptr;
+    if (S->n_b > 0 && S->geom_static_after > 0.0 && !std::getenv("IBMGPU_FULL_REFRESH"))
+        S->rcache.init(c, S->G, S->BN, S->lhs2, S->n_p, 0, S->n_order);
     lap("E, H, Q, Q^T, lhs2");
     for (Mat* m : {S->L, S->A, S->BN, S->G}) mat_plan(c, m);
     lap("SpMV plans");
@@ -898,7 +943,12 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
     }
     // stage 2 (single GPU: one graph launch; distributed: row-slab PCG, dist.cu)
     if (distributed) S->ensure_dist();
+    static const bool prof = std::getenv("IBMGPU_SETUP_PROFILE") != nullptr;
+    const auto tp0 = clk::now();
     PcgPlan* P2 = distributed ? nullptr : pcg_plan(c, S->lhs2, IBMGPU_PC_SA, S->hier);
+    if (prof)
+        std::fprintf(stderr, "[step] solve-2 plan %8.3f ms\n",
+                     std::chrono::duration<double, std::milli>(clk::now() - tp0).count());
     double* b2 = distributed ? S->b2.p : P2->b.p;
     double* lam = distributed ? S->x2.p : P2->x.p;
     const Bc2 bc2{S->bl, S->bnd.p, S->dx.p, S->dy.p};
@@ -1110,7 +1160,7 @@ int ibmgpu_stepper_forces(ibmgpu_stepper_t S, double* out4) {
 int ibmgpu_stepper_op(ibmgpu_stepper_t S, const char* name, ibmgpu_mat_t* out) {
     return sguard(S, [&] {
         const std::string n(name);
-        Mat* m = n == "L" ? S->L : n == "G" ? S->G : n == "E" ? S->E : n == "H" ? S->H : n == "A" ? S->A
+        Mat* m = n == "L" ? S->L : n == "G" ? S->G : n == "E" ? S->E : n == "H" ? S->ensure_H() : n == "A" ? S->A
                : n == "BN" ? S->BN : n == "Q" ? S->Q : n == "QT" ? S->QT : n == "lhs2" ? S->lhs2 : nullptr;
         require(m != nullptr, "stepper_op: unknown operator " + n);
         m->borrowed = true;
