@@ -17,6 +17,7 @@
 #include <cub/cub.cuh>
 
 #include <atomic>
+#include <future>
 #include <chrono>
 #include <cstdio>
 #include <cmath>
@@ -888,6 +889,83 @@ int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& 
 }
 
 
+// k_smooth_p with one thread per row, for rows of at most kThreadCap core entries (level 0:
+// at most 16); a longer row sets *over and the warp kernel runs instead
+constexpr int kThreadCap = 24;
+__global__ void k_smooth_p_thread(int rows, int n_core, int n_agg, double omega, const int* __restrict__ arp,
+                                  const int* __restrict__ aci, const double* __restrict__ av,
+                                  const double* __restrict__ invd, const int* __restrict__ agg,
+                                  const int* __restrict__ size, int* __restrict__ cnt, const int* __restrict__ orp,
+                                  int* __restrict__ oci, double* __restrict__ ov, int* __restrict__ over) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    if (i >= n_core) {
+        if (cnt) {
+            cnt[i] = 1;
+        } else {
+            oci[orp[i]] = n_agg + (i - n_core);
+            ov[orp[i]] = 1.0;
+        }
+        return;
+    }
+    int col[kThreadCap + 1];
+    double val[kThreadCap + 1];
+    int n = 0;
+    const double di = invd[i];
+    for (int k = arp[i]; k < arp[i + 1]; ++k) {
+        const int kk = aci[k];
+        if (kk >= n_core) continue;  // P_tent's tail rows are empty
+        if (n == kThreadCap) {
+            *over = 1;
+            return;
+        }
+        const int a = agg[kk];
+        const double p = mul(mul(av[k], di), ptent_val(size, a));
+        // Gustavson: the first product of a column starts from 0.0, later ones add in A-row order
+        int t = 0;
+        while (t < n && col[t] != a) ++t;
+        if (t < n) {
+            val[t] = addd(val[t], p);
+        } else {
+            col[n] = a;
+            val[n] = addd(0.0, p);
+            ++n;
+        }
+    }
+    // the P_tent entry of the row's own aggregate, then columns in increasing order
+    const int ai = agg[i];
+    const double pti = addd(0.0, mul(1.0, ptent_val(size, ai)));
+    bool has_ai = false;
+    for (int t = 0; t < n; ++t) has_ai |= col[t] == ai;
+    if (!has_ai) {
+        col[n] = ai;
+        val[n] = 0.0;  // marker: no DAP entry (handled below)
+    }
+    const int total = n + (has_ai ? 0 : 1);
+    int outn = 0;
+    const int o = cnt ? 0 : orp[i];
+    int last = -1;
+    for (int q = 0; q < total; ++q) {
+        int best = -1;  // next column above `last` (selection: rows are short)
+        for (int t = 0; t < total; ++t)
+            if (col[t] > last && (best < 0 || col[t] < col[best])) best = t;
+        last = col[best];
+        double v;
+        if (best == n)  // P_tent only
+            v = pti;
+        else
+            v = addd(col[best] == ai ? pti : 0.0, mul(-omega, val[best]));
+        if (v != 0.0) {
+            if (!cnt) {
+                oci[o + outn] = col[best];
+                ov[o + outn] = v;
+            }
+            ++outn;
+        }
+    }
+    if (cnt) cnt[i] = outn;
+}
+
 // P in one fused pass (k_smooth_p); nullptr when a row is too long for it
 Mat* smoothed_prolongator(Ctx* c, const Mat* A, const double* invd, const int* agg, const int* size, int n_core,
                           int n_agg, double omega) {
@@ -895,12 +973,22 @@ Mat* smoothed_prolongator(Ctx* c, const Mat* A, const double* invd, const int* a
     DBuf<int> cnt(c, (size_t)rows + 1), over(c, 1);
     CK(cudaMemsetAsync(over.p, 0, sizeof(int), c->stream));
     const int grid = std::max(1, std::min(blocks(rows, kSmallWarps), c->num_sms * 8));
-    k_smooth_p<<<grid, kSmallWarps * 32, 0, c->stream>>>(rows, n_core, n_agg, omega, A->rp.p, A->ci.p, A->v.p, invd,
-                                                         agg, size, cnt.p, nullptr, nullptr, nullptr, over.p);
+    int hv[2];
+    // thread per row first; the warp kernel when some row is longer than kThreadCap
+    bool thread = true;
+    k_smooth_p_thread<<<blocks(rows), 256, 0, c->stream>>>(rows, n_core, n_agg, omega, A->rp.p, A->ci.p, A->v.p,
+                                                           invd, agg, size, cnt.p, nullptr, nullptr, nullptr, over.p);
     CK_LAUNCH(c);
+    hv[0] = d2h_scalar(c, over.p);
+    if (hv[0]) {
+        thread = false;
+        CK(cudaMemsetAsync(over.p, 0, sizeof(int), c->stream));
+        k_smooth_p<<<grid, kSmallWarps * 32, 0, c->stream>>>(rows, n_core, n_agg, omega, A->rp.p, A->ci.p, A->v.p,
+                                                             invd, agg, size, cnt.p, nullptr, nullptr, nullptr, over.p);
+        CK_LAUNCH(c);
+    }
     Mat* P = mat_new(c, rows, n_agg + tail, 0);
     exclusive_scan_total(c, cnt.p, P->rp.p, rows);
-    int hv[2];
     d2h(c, hv, over.p, 1);
     d2h(c, hv + 1, P->rp.p + rows, 1);
     sync(c);
@@ -911,11 +999,39 @@ Mat* smoothed_prolongator(Ctx* c, const Mat* A, const double* invd, const int* a
     P->nnz = hv[1];
     P->ci.alloc(c, (size_t)std::max(P->nnz, 1));
     P->v.alloc(c, (size_t)std::max(P->nnz, 1));
-    k_smooth_p<<<grid, kSmallWarps * 32, 0, c->stream>>>(rows, n_core, n_agg, omega, A->rp.p, A->ci.p, A->v.p, invd,
-                                                         agg, size, nullptr, P->rp.p, P->ci.p, P->v.p, over.p);
+    if (thread)
+        k_smooth_p_thread<<<blocks(rows), 256, 0, c->stream>>>(rows, n_core, n_agg, omega, A->rp.p, A->ci.p, A->v.p,
+                                                               invd, agg, size, nullptr, P->rp.p, P->ci.p, P->v.p,
+                                                               over.p);
+    else
+        k_smooth_p<<<grid, kSmallWarps * 32, 0, c->stream>>>(rows, n_core, n_agg, omega, A->rp.p, A->ci.p, A->v.p,
+                                                             invd, agg, size, nullptr, P->rp.p, P->ci.p, P->v.p,
+                                                             over.p);
     CK_LAUNCH(c);
     return P;
 }
+
+// A second stream (and context view of the same device) for setup work that runs beside the
+// main stream's critical path.
+struct AuxStream {
+    Ctx c;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    explicit AuxStream(Ctx* main) {
+        c.device = main->device;
+        c.num_sms = main->num_sms;
+        c.eager = main->eager;
+        CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    }
+    ~AuxStream() {
+        cudaStreamSynchronize(c.stream);
+        cudaEventDestroy(fork);
+        cudaEventDestroy(join);
+        cudaStreamDestroy(c.stream);
+        c.stream = nullptr;
+    }
+};
 
 Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o, AggCache* cache) {
     require(A_fine->rows == A_fine->cols, "sa: square matrix required");
@@ -925,6 +1041,7 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o, AggCache* cac
     h->id = next_id++;
     try {
         const int tail = std::min(o.keep_fine_tail, A_fine->rows);
+        AuxStream aux(c);
         // level-0 A is a private copy (the hierarchy owns every level, as SaLevel::A does)
         Mat* A = scale(c, A_fine, 0, 1.0, nullptr);
         for (int lev = 0; lev < o.max_levels && A->rows > o.max_coarse + tail; ++lev) {
@@ -932,14 +1049,6 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o, AggCache* cac
             const int n_core = A->rows - tail;
             auto L = std::make_unique<Level>();
             if (cache && cache->lv.size() <= (size_t)lev) cache->lv.resize(lev + 1);
-            bool hit = false;
-            const int n_agg = aggregate_device(c, A, theta_l, n_core, L->agg, cache ? &cache->lv[lev] : nullptr, &hit);
-            if (cache) ++(hit ? cache->hits : cache->misses);
-            clk.lap("aggregate", lev);
-            if (n_agg >= n_core) {
-                h->stalled = true;
-                break;
-            }
             const int n = A->rows;
             DBuf<double> d(c, (size_t)n);
             diag_of(c, A, d.p);
@@ -948,13 +1057,41 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o, AggCache* cac
             CK(cudaMemsetAsync(zero.p, 0, sizeof(int), c->stream));
             k_invd<<<blocks(n), 256, 0, c->stream>>>(n, d.p, 0.0, L->invd.p, nullptr, zero.p);
             CK_LAUNCH(c);
+            // The power iteration (amg.hpp:58-75, with this level's SpMV plan) only needs A and
+            // 1/diag, the aggregation (amg.hpp:79-123) only A: they run concurrently, the power
+            // iteration from a helper thread on the aux stream. Same kernels, same results.
+            CK(cudaEventRecord(aux.fork, c->stream));
+            CK(cudaStreamWaitEvent(aux.c.stream, aux.fork, 0));
+            const double* invd_p = L->invd.p;
+            auto rho_f = std::async(std::launch::async, [&aux, A, invd_p, &o, dev = c->device] {
+                CK(cudaSetDevice(dev));
+                return rho_dinv_a(&aux.c, A, invd_p, o.power_iterations);
+            });
+            bool hit = false;
+            int n_agg = 0;
+            try {
+                n_agg = aggregate_device(c, A, theta_l, n_core, L->agg, cache ? &cache->lv[lev] : nullptr, &hit);
+            } catch (...) {
+                rho_f.wait();
+                throw;
+            }
+            const double rho = rho_f.get();
+            c->launches += aux.c.launches;
+            aux.c.launches = 0;
+            CK(cudaEventRecord(aux.join, aux.c.stream));
+            CK(cudaStreamWaitEvent(c->stream, aux.join, 0));
+            mat_rehome(A, c->stream);  // its SpMV plan was built on the aux stream
+            if (cache) ++(hit ? cache->hits : cache->misses);
+            clk.lap("aggregate+rho", lev);
+            if (n_agg >= n_core) {
+                h->stalled = true;
+                break;
+            }
             if (d2h_scalar(c, zero.p)) {
                 delete A;
                 fail(IBMGPU_EINVAL, "sa: zero diagonal");
             }
-            const double rho = rho_dinv_a(c, A, L->invd.p, o.power_iterations);
             const double omega = (4.0 / 3.0) / rho;
-            clk.lap("rho", lev);
             L->wd.alloc(c, (size_t)n);
             k_invd<<<blocks(n), 256, 0, c->stream>>>(n, d.p, omega, L->invd.p, L->wd.p, zero.p);
             CK_LAUNCH(c);

@@ -155,6 +155,17 @@ struct ibmgpu_mat {
 namespace ibmgpu {
 using Mat = ibmgpu_mat;
 
+// Device buffers are freed on the stream they were allocated on; a matrix planned on a helper
+// stream is handed back to the main stream with this before anything else uses it.
+inline void mat_rehome(Mat* m, cudaStream_t s) {
+    auto set = [s](auto& b) {
+        if (b.p) b.s = s;
+    };
+    set(m->rp), set(m->ci), set(m->v), set(m->sell_off), set(m->sell_ci), set(m->sell_v), set(m->perm);
+    set(m->long_rows), set(m->st_v), set(m->st_mask), set(m->st_erp), set(m->st_eci), set(m->st_ev);
+    set(m->blk_meta), set(m->lrow), set(m->lpart), set(m->lcnt);
+}
+
 // csr.cu
 Mat* mat_new(Ctx* c, int rows, int cols, int nnz);
 void mat_plan(Ctx* c, Mat* m);              // build the SpMV plan (SELL copy or vector width)

@@ -462,6 +462,7 @@ Mat* finish_plan(Ctx*, Mat* m) { return m; }
 // the reference accumulates it. Columns are then sorted (bitonic, in shared memory). Symbolic
 // pass: unique counts per row; a row over 3/4 of the symbolic table sends the product to ESC.
 constexpr int kHashSym = 4096, kSymWarps = 8;
+constexpr int kHashU = 4;  // product batches whose loads are issued together
 
 __device__ __forceinline__ unsigned hslot(int c, int mask) { return ((unsigned)c * 2654435761u) & (unsigned)mask; }
 
@@ -541,12 +542,22 @@ __global__ void __launch_bounds__(kSymWarps * 32) k_hash_symbolic(int r0, int ro
         for (int c0 = b; c0 < e; c0 += 32) {
             if (*(volatile int*)(counter + w) > kHashSym * 3 / 4) break;  // overflow: ESC takes over
             const int total = chunk_load(ch, c0, e, aci, nullptr, brp, lane, false);
-            for (int q0 = 0; q0 < total; q0 += 32) {
+            for (int q0 = 0; q0 < total; q0 += 32 * kHashU) {
                 if (*(volatile int*)(counter + w) > kHashSym * 3 / 4) break;
-                const int q = q0 + lane;
-                if (q < total) {
-                    const int o = chunk_owner(ch, q);
-                    const int col = __ldg(bci + ch.bs[o] + (q - ch.off[o]));
+                int cols[kHashU];  // kHashU independent column loads in flight per lane
+#pragma unroll
+                for (int u = 0; u < kHashU; ++u) {
+                    const int q = q0 + u * 32 + lane;
+                    cols[u] = -1;
+                    if (q < total) {
+                        const int o = chunk_owner(ch, q);
+                        cols[u] = __ldg(bci + ch.bs[o] + (q - ch.off[o]));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kHashU; ++u) {
+                    const int col = cols[u];
+                    if (col < 0) continue;
                     unsigned h = hslot(col, kHashSym - 1);
                     for (int probe = 0; probe < kHashSym; ++probe) {
                         const int prev = atomicCAS(keys + h, -1, col);
@@ -597,31 +608,43 @@ __global__ void k_hash_numeric(int r0, int rows, const int* __restrict__ arp, co
         const int i = r0 + row, b = __ldg(arp + i), e = __ldg(arp + i + 1);
         for (int c0 = b; c0 < e; c0 += 32) {
             const int total = chunk_load(ch, c0, e, aci, av, brp, lane, true);
-            for (int q0 = 0; q0 < total; q0 += 32) {
-                const int q = q0 + lane;
-                int col = -1;
-                double p = 0.0;
-                if (q < total) {
-                    const int o = chunk_owner(ch, q);
-                    const int jj = ch.bs[o] + (q - ch.off[o]);
-                    col = __ldg(bci + jj);
-                    p = mul(ch.a[o], __ldg(bv + jj));
-                }
-                prod[lane] = p;
-                const unsigned grp = __match_any_sync(kFull, col);
-                __syncwarp();
-                if (col >= 0 && lane == __ffs(grp) - 1) {
-                    unsigned h = hslot(col, mask);
-                    for (;;) {  // find or claim the column's slot (other leaders hold other columns)
-                        const int prev = atomicCAS(keys + h, -1, col);
-                        if (prev == -1 || prev == col) break;
-                        h = (h + 1) & mask;
+            for (int q0 = 0; q0 < total; q0 += 32 * kHashU) {
+                // kHashU batches of 32 products loaded at once (independent loads in flight),
+                // then accumulated batch by batch: Gustavson order is kept
+                int cols[kHashU];
+                double ps[kHashU];
+#pragma unroll
+                for (int u = 0; u < kHashU; ++u) {
+                    const int q = q0 + u * 32 + lane;
+                    cols[u] = -1;
+                    ps[u] = 0.0;
+                    if (q < total) {
+                        const int o = chunk_owner(ch, q);
+                        const int jj = ch.bs[o] + (q - ch.off[o]);
+                        cols[u] = __ldg(bci + jj);
+                        ps[u] = mul(ch.a[o], __ldg(bv + jj));
                     }
-                    double acc = vals[h];
-                    for (unsigned m = grp; m; m &= m - 1) acc = addd(acc, prod[__ffs(m) - 1]);
-                    vals[h] = acc;
                 }
-                __syncwarp();
+#pragma unroll
+                for (int u = 0; u < kHashU; ++u) {
+                    if (q0 + u * 32 >= total) break;  // warp-uniform
+                    const int col = cols[u];
+                    prod[lane] = ps[u];
+                    const unsigned grp = __match_any_sync(kFull, col);
+                    __syncwarp();
+                    if (col >= 0 && lane == __ffs(grp) - 1) {
+                        unsigned h = hslot(col, mask);
+                        for (;;) {  // find or claim the column's slot (other leaders hold other columns)
+                            const int prev = atomicCAS(keys + h, -1, col);
+                            if (prev == -1 || prev == col) break;
+                            h = (h + 1) & mask;
+                        }
+                        double acc = vals[h];
+                        for (unsigned m = grp; m; m &= m - 1) acc = addd(acc, prod[__ffs(m) - 1]);
+                        vals[h] = acc;
+                    }
+                    __syncwarp();
+                }
             }
             __syncwarp();
         }
