@@ -7,8 +7,14 @@ SRC := $(wildcard $(PKG)/csrc/*.cu)
 HOST := $(wildcard $(PKG)/csrc/host/*.cpp)
 HDR := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/host/*.hpp) include/ibmgpu.h
 OBJDIR := build/obj
+# make CHECKED=1: device-side bounds checks (IBM_DCHECK traps) — the stand-in for compute-sanitizer,
+# which is closed on the GPU pool; run the GPU tests against this build (tools/checked_run.sh)
+ifeq ($(CHECKED),1)
+CHECKFLAGS := -DIBMGPU_CHECKED=1
+OBJDIR := build/obj_checked
+endif
 OBJ := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(SRC)) $(patsubst $(PKG)/csrc/host/%.cpp,$(OBJDIR)/host_%.o,$(HOST))
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC,-fopenmp -Xptxas -v --expt-relaxed-constexpr
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC,-fopenmp -Xptxas -v --expt-relaxed-constexpr $(CHECKFLAGS)
 HOSTFLAGS := -O3 -std=c++20 -fPIC -fopenmp -ffp-contract=off
 
 all: $(PKG)/libibmgpu.so oracle

@@ -453,7 +453,10 @@ __global__ void k_pass3(int n, int base, const int* __restrict__ flag, const int
 // ---------------------------------------------------------------- prolongator pieces
 __global__ void k_agg_size(int n, const int* __restrict__ agg, int* __restrict__ size) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) atomicAdd(size + agg[i], 1);
+    if (i < n) {
+        IBM_DCHECK(agg[i] >= 0);  // pass 3 leaves no row unassigned
+        atomicAdd(size + agg[i], 1);
+    }
 }
 
 // P_tent (amg.hpp:156-161): rows < n_core hold (agg[i], 1/sqrt(|agg|)); tail rows empty

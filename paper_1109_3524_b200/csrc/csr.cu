@@ -38,6 +38,7 @@ void exclusive_scan_total(Ctx* c, const int* in, int* out, int n) {
     CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, in, out + 1, n, c->stream));
     DBuf<char> t(c, tmp);
     CK(cub::DeviceScan::InclusiveSum(t.p, tmp, in, out + 1, n, c->stream));
+    c->pdl_fence = 1;  // library kernels write too (CK_LAUNCH)
 }
 
 long long exclusive_scan_total64(Ctx* c, const long long* in, long long* out, int n) {
@@ -47,6 +48,7 @@ long long exclusive_scan_total64(Ctx* c, const long long* in, long long* out, in
     CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, in, out + 1, n, c->stream));
     DBuf<char> t(c, tmp);
     CK(cub::DeviceScan::InclusiveSum(t.p, tmp, in, out + 1, n, c->stream));
+    c->pdl_fence = 1;  // library kernels write too (CK_LAUNCH)
     return d2h_scalar(c, out + n);
 }
 

@@ -31,10 +31,16 @@ inline void require(bool ok, const std::string& msg) {
                                std::to_string(__LINE__) + ")");                                         \
     } while (0)
 
+// Every plain <<<>>> launch goes through CK_LAUNCH, which raises the context's PDL fence: the
+// next launch_k (kern.cuh) then runs without programmatic stream serialization. Plain launches
+// are where matrices and plans get written (assembly, SpGEMM, plan fills), and the PDL SpMV
+// kernels read their constant matrix BEFORE griddepcontrol.wait — the fence guarantees they
+// never overlap the kernel that wrote it.
 #define CK_LAUNCH(ctx)                 \
     do {                               \
         CK(cudaGetLastError());        \
         ++(ctx)->launches;             \
+        (ctx)->pdl_fence = 1;          \
     } while (0)
 
 }  // namespace ibmgpu
@@ -50,6 +56,7 @@ struct ibmgpu_ctx {
     void* nccl = nullptr;       // ncclComm_t when nranks > 1
     void* pcg_cache = nullptr;  // pcg.cu plan cache
     int eager = 0;              // IBMGPU_EAGER=1: host-looped solves (profiling only)
+    int pdl_fence = 0;          // set by plain launches: the next launch_k skips PDL (CK_LAUNCH)
 };
 
 namespace ibmgpu {

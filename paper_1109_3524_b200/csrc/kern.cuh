@@ -19,6 +19,19 @@ __device__ __forceinline__ double addd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double subd(double a, double b) { return __dsub_rn(a, b); }
 
 constexpr int kBlock = 256;
+
+// Device-side invariant checks of the checked build (make CHECKED=1): a violated bound traps the
+// kernel (cudaErrorIllegalInstruction at the next sync), so the test that ran it fails loudly.
+#if defined(IBMGPU_CHECKED)
+#define IBM_DCHECK(cond)        \
+    do {                        \
+        if (!(cond)) __trap();  \
+    } while (0)
+#else
+#define IBM_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
 constexpr unsigned kFull = 0xffffffffu;
 
 // L1 prefetch of an epilogue operand, issued before the row loop so its DRAM latency overlaps
@@ -63,7 +76,11 @@ inline void launch_k(Ctx* c, void (*kernel)(KArgs...), int grid, int block, cuda
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    // PDL invariant: SpMV kernels load their matrix before griddepcontrol.wait, which is only
+    // safe when the predecessor did not write it; after any plain launch (CK_LAUNCH sets the
+    // fence) this launch waits for full completion instead
+    cfg.numAttrs = pdl_enabled() && !c->pdl_fence ? 1 : 0;
+    c->pdl_fence = 0;
     CK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
     ++c->launches;
 }

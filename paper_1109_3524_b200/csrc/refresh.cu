@@ -114,6 +114,7 @@ __global__ void k_merge(int n, int n_p, int pin, const int* __restrict__ lrp, co
         for (int k = srp[i]; k < srp[i + 1]; ++k) {
             const int col = sci[k];
             if (col == pin) continue;
+            IBM_DCHECK(i >= n_p || col >= n_p);  // the cached pressure block holds every pressure column
             if (oci) {
                 oci[o + m] = col;
                 ov[o + m] = sv[k];

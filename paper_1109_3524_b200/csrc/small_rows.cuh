@@ -26,6 +26,7 @@ __device__ __forceinline__ int small_expand(SmallRow& w, const int* ci, const do
         const int kk = ci[k];
         const double a = v[k];
         const int s = mrp[kk], len = mrp[kk + 1] - s;
+        IBM_DCHECK(n + len <= kSmallCap);
         for (int t = lane; t < len; t += 32) {  // B-row order
             w.col[n + t] = mci[s + t];
             w.val[n + t] = mul(a, mv[s + t]);

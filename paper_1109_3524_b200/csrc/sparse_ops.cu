@@ -330,6 +330,7 @@ void sort_pairs(Ctx* c, unsigned long long* kin, unsigned long long* kout, doubl
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, n, 0, end_bit, c->stream));
     DBuf<char> t(c, tmp);
     CK(cub::DeviceRadixSort::SortPairs(t.p, tmp, kin, kout, vin, vout, n, 0, end_bit, c->stream));
+    c->pdl_fence = 1;
 }
 
 // Segment bookkeeping over sorted keys: returns number of unique keys; fills start[u].
@@ -342,6 +343,7 @@ int segments(Ctx* c, const unsigned long long* keys, long long n, DBuf<long long
     CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, head.p, uid.p, (int)n, c->stream));
     DBuf<char> t(c, tmp);
     CK(cub::DeviceScan::ExclusiveSum(t.p, tmp, head.p, uid.p, (int)n, c->stream));
+    c->pdl_fence = 1;
     const int last_uid = d2h_scalar(c, uid.p + n - 1);
     const int last_head = d2h_scalar(c, head.p + n - 1);
     const int n_unique = last_uid + last_head;
@@ -634,10 +636,12 @@ __global__ void k_hash_numeric(int r0, int rows, const int* __restrict__ arp, co
                     __syncwarp();
                     if (col >= 0 && lane == __ffs(grp) - 1) {
                         unsigned h = hslot(col, mask);
+                        int probes = 0;
                         for (;;) {  // find or claim the column's slot (other leaders hold other columns)
                             const int prev = atomicCAS(keys + h, -1, col);
                             if (prev == -1 || prev == col) break;
                             h = (h + 1) & mask;
+                            IBM_DCHECK(++probes < slots);  // table never full
                         }
                         double acc = vals[h];
                         for (unsigned m = grp; m; m &= m - 1) acc = addd(acc, prod[__ffs(m) - 1]);
@@ -686,7 +690,9 @@ __global__ void k_hash_numeric(int r0, int rows, const int* __restrict__ arp, co
                 __syncwarp();
             }
         const int o0 = crp[row];
+        IBM_DCHECK(o0 + n_u == crp[row + 1]);  // symbolic count == numeric count
         for (int t = lane; t < n_u; t += 32) {
+            IBM_DCHECK(keys[t] >= 0 && (t == 0 || keys[t - 1] < keys[t]));  // unique, sorted columns
             cci[o0 + t] = keys[t];
             cv[o0 + t] = vals[t];
         }
@@ -846,6 +852,7 @@ Mat* transpose(Ctx* c, const Mat* A) {
         CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, A->ci.p, kout.p, idx.p, perm.p, A->nnz, 0, eb, c->stream));
         DBuf<char> tt(c, tmp);
         CK(cub::DeviceRadixSort::SortPairs(tt.p, tmp, A->ci.p, kout.p, idx.p, perm.p, A->nnz, 0, eb, c->stream));
+        c->pdl_fence = 1;
         k_transpose_fill<<<blocks(A->nnz), 256, 0, c->stream>>>(A->nnz, perm.p, row_of.p, A->v.p, t->ci.p, t->v.p);
         CK_LAUNCH(c);
     }

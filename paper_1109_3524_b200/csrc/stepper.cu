@@ -32,6 +32,8 @@
 #include "pcg.cuh"
 #include "refresh.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace ibmgpu {
 struct GridDev;
 GridDev* grid_dev_new(Ctx* c, const ibm_grid_desc& g);
@@ -861,7 +863,17 @@ void set_err(ibm_step_report* rep, const std::string& m) {
 std::string fmt_res(double r) { return std::to_string(r); }
 
 // Stepper::advance (stepper.hpp:231-356)
+// NVTX range per phase of Stepper::advance (stepper.hpp:232-321): visible in any CUDA profiler
+// timeline (nsys / ncu --nvtx); the ranges cover the host enqueue of each phase
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
+    NvtxRange step_range("ibm.advance");
     Ctx* c = S->c;
     using clk = std::chrono::steady_clock;
     std::memset(rep, 0, sizeof(*rep));
@@ -872,6 +884,7 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
     auto tic = clk::now();
     if (moving) {
         try {
+            NvtxRange r("refresh_body_operators");
             S->refresh_body_operators();
         } catch (const Error& e) {
             if (e.code == IBMGPU_ESUPPORT) {
@@ -886,6 +899,7 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
         tic = clk::now();
         const bool freezing = t_new >= S->geom_static_after;
         if (S->force_rebuild || freezing || S->step % S->n_pc == 0) {
+            NvtxRange r("build_sa_hierarchy");
             S->rebuild_hierarchy();
             S->hier->built_at_step = S->step;
             rep->rebuilt_hierarchy = 1;
@@ -900,6 +914,7 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
     CK(cudaEventRecord(S->ev[0], s));
     CK(cudaMemsetAsync(S->sd.p, 0, sizeof(StepDev), s));
     // explicit terms
+    nvtxRangePushA("explicit terms + rhs1");
     const GridArrays ga{S->dx.p, S->dy.p, S->del_x.p, S->del_y.p};
     k_bc_update<<<1, 1024, 0, s>>>(S->bl, ga, S->ek, S->q.p, S->bnd.p, S->bnd_n.p, &S->sd.p->bc_err);
     CK_LAUNCH(c);
@@ -922,6 +937,8 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
                         qs},
                 s);
     CK(cudaEventRecord(S->ev[1], s));
+    nvtxRangePop();
+    nvtxRangePushA("solve 1 (pcg-diag)");
     ibm_solve_result r1;
     if (distributed) {
         dist_solve(S->dist1, b1, qs, S->p1, &r1, nullptr);
@@ -933,6 +950,7 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
     }
     if (d2h_scalar(c, &S->sd.p->bc_err))
         fail(IBMGPU_ECUDA, "boundary: prescribed velocities have nonzero net flux and no convective edge to absorb it");
+    nvtxRangePop();
     rep->solve1_iters = r1.iterations;
     rep->solve1_res = r1.rel_residual;
     rep->bc_cfl = S->max_cfl;
@@ -942,6 +960,7 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
         return;
     }
     // stage 2 (single GPU: one graph launch; distributed: row-slab PCG, dist.cu)
+    nvtxRangePushA("solve 2 (rhs2 + pcg-sa)");
     if (distributed) S->ensure_dist();
     static const bool prof = std::getenv("IBMGPU_SETUP_PROFILE") != nullptr;
     const auto tp0 = clk::now();
@@ -964,6 +983,7 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
         CK(cudaEventRecord(S->ev[4], s));
         P2->finish(c, &r2);
     }
+    nvtxRangePop();
     rep->solve2_iters = r2.iterations;
     rep->solve2_res = r2.rel_residual;
     if (r2.status != 0) {
@@ -971,6 +991,7 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
         return;
     }
     // stage 3: projection q = q* - B^N (Q lambda)
+    NvtxRange proj_range("projection + invariants");
     if (S->bn_diagonal) {
         launch_spmv(c, S->Q, XPlain{lam}, EpiProjectDiag{qs, S->bn_diag.p, S->q_new.p, &S->sd.p->nonfinite}, s);
     } else {
