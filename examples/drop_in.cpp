@@ -43,7 +43,7 @@ int main(int argc, char** argv) {
         write_checkpoint("/tmp/ibm_b200_drop_in.ckpt", st);
         Stepper resumed(argv[1]);
         read_checkpoint("/tmp/ibm_b200_drop_in.ckpt", resumed);
-        const bool same = st.advance().ok && resumed.advance().ok && st.q() == resumed.q();
+        const bool same = st.advance().ok && resumed.advance().ok && st.state().q == resumed.state().q;
         std::printf("checkpoint resume %s\n", same ? "bitwise identical" : "DIFFERS");
         if (!same) return 1;
     }

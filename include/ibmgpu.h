@@ -1,7 +1,7 @@
 /* ibmgpu.h — C-ABI of the B200-native IBPM sparse linear-algebra hot path.
  *
  * Drop-in boundary for the reference's in-process operator API
- * (/root/reference/proj/include/ibm/*.hpp; the reference is header-only C++ with no FFI,
+ * (/root/reference/proj/include/ibm/<name>.hpp; the reference is header-only C++ with no FFI,
  * so each entry point below names the C++ function/method it replaces). Plain pointers
  * and sizes only; no torch or CUDA types in any signature. `*_dev` arguments are device
  * pointers obtained from ibmgpu_vec_alloc (or any cudaMalloc'd memory on the context's
@@ -226,6 +226,85 @@ int ibmgpu_stepper_bodies(ibmgpu_stepper_t st, double* x, double* y, double* ubx
 int ibmgpu_stepper_vorticity(ibmgpu_stepper_t st, double* out, int* n);
 /* time the last advance() spent in each device phase, from CUDA events (ms) */
 int ibmgpu_stepper_phase_ms(ibmgpu_stepper_t st, float* ms6);
+
+/* ---------------------------------------------------------------- reference-shaped construction
+ * Stepper(grid, bodies, bc, nu, params, u0, v0) (stepper.hpp:171-195) and assemble_operators
+ * (operators.hpp:420-442) from in-memory objects instead of a case file; the C++ shim
+ * (ibm_b200.hpp) builds these descriptors from its StaggeredGrid / LagrangianBody / BcSpec /
+ * SteppingParams, the reference's own types. */
+typedef struct {
+    int kind; /* BcKind: 0 dirichlet, 1 convective (boundary.hpp:15-21) */
+    double u, v;
+} ibm_edge_bc;
+typedef struct {
+    ibm_edge_bc left, right, bottom, top;
+    double u_inf;
+} ibm_bc_spec; /* BcSpec (boundary.hpp:23-32) */
+typedef struct {
+    int n_points;
+    const double *ref_x, *ref_y; /* shape about the centroid (LagrangianBody::ref_x/ref_y) */
+    double center_x, center_y, ds;
+    int motion; /* MotionKind: 0 stationary, 1 rotating, 2 heaving, 3 flapping (body.hpp:30-63) */
+    double omega, k, kh, heave_omega, heave_amp, A0, f, alpha0, beta, phase;
+    int shape_rotation_invariant;
+    double preamble_offset, preamble_duration;
+} ibm_body_desc; /* LagrangianBody (body.hpp:85-148) */
+typedef struct {
+    double dt;
+    int n_order, n_pc, force_rebuild, slice_rows;
+    ibm_solver_params solve1, solve2;
+    ibm_sa_options sa;
+} ibm_stepping_params; /* SteppingParams (stepper.hpp:110-125) */
+
+/* Stepper::Stepper (stepper.hpp:171-195). The grid's domain is its first/last faces. */
+int ibmgpu_stepper_create_from(ibmgpu_ctx_t ctx, const ibm_grid_desc* grid, int n_bodies,
+                               const ibm_body_desc* bodies, const ibm_bc_spec* bc, double nu,
+                               const ibm_stepping_params* params, double u0, double v0, ibmgpu_stepper_t* out);
+/* assemble_operators (operators.hpp:420-442): the returned stepper handle holds only the operator
+ * set (read with ibmgpu_stepper_op; advance is refused) */
+int ibmgpu_operators_create(ibmgpu_ctx_t ctx, const ibm_grid_desc* grid, int n_bodies, const ibm_body_desc* bodies,
+                            double dt, double nu, int n_order, int pin, int slice_rows, ibmgpu_stepper_t* out);
+
+/* pcg (krylov.hpp:70-136) with a caller-supplied preconditioner — the reference's polymorphic
+ * Preconditioner::apply (krylov.hpp:39-43). apply(user, n, r_dev, z_dev) must write z = M^{-1} r
+ * (device pointers, context stream order; it may launch its own kernels or copy through the
+ * host) and return 0, or nonzero to abort the solve with IBMGPU_EINVAL. */
+typedef int (*ibmgpu_apply_fn)(void* user, int n, const double* r_dev, double* z_dev);
+int ibmgpu_pcg_callback(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, ibmgpu_apply_fn apply, void* user, const double* b_dev,
+                        double* x_inout_dev, const ibm_solver_params* params, ibm_solve_result* result,
+                        double* history_host);
+
+/* host-only builders (no CUDA; the reference's grid.hpp / body.hpp / config.hpp functions).
+ * Two-phase: call with NULL outputs to get the sizes. err: message on failure. */
+/* build_stretched_grid (grid.hpp:148-192): packed = x_faces, y_faces, dx, dy, x_c, y_c, del_x,
+ * del_y (lengths nx+1, ny+1, nx, ny, nx, ny, nx-1, ny-1); uniform4 = snapped uniform region */
+int ibmgpu_host_grid(const double domain[4], const double uniform[4], double h_min, const double ratio[4], int* nx,
+                     int* ny, double* packed, double* uniform4, char* err, int err_cap);
+/* discretize_circle / discretize_ellipse (body.hpp:151-261) */
+int ibmgpu_host_circle(double cx, double cy, double diameter, double h, int* n, double* ref_x, double* ref_y,
+                       double* ds, char* err, int err_cap);
+int ibmgpu_host_ellipse(double cx, double cy, double chord, double thickness_ratio, double h, int n_override, int* n,
+                        double* ref_x, double* ref_y, double* ds, char* err, int err_cap);
+/* the scalar part of CaseConfig (config.hpp:54-95) as parse_config reads it */
+typedef struct {
+    int kind; /* SolverKind: 0 cg, 1 pcg-diag, 2 pcg-sa, 3 amg */
+    double rel_tol;
+    int max_iters;
+    double sa_theta;
+    int sa_max_coarse;
+} ibm_solver_config;
+typedef struct {
+    double domain[4], uniform[4], h_min, ratio[4];
+    double nu, re, u_inf, ref_length, u0, v0, dt;
+    int n_steps, n_out, checkpoint_every, n_pc, n_order, slice_rows, n_bodies;
+    ibm_bc_spec bc;
+    ibm_solver_config solve1, solve2;
+    char out_dir[512];
+} ibm_case_config;
+int ibmgpu_host_case_config(const char* cfg_path, ibm_case_config* out, char* err, int err_cap);
+/* build_bodies (config.hpp:358-385): descs[k].ref_x/ref_y point into xy (2 * n_points_total) */
+int ibmgpu_host_case_bodies(const char* cfg_path, int* n_bodies, int* n_points_total, ibm_body_desc* descs,
+                            double* xy, char* err, int err_cap);
 
 /* ---------------------------------------------------------------- host-only case setup
  * The host half of case loading (config.hpp parse_config, grid.hpp build_stretched_grid,

@@ -290,6 +290,14 @@ int ibmgpu_pcg(ibmgpu_ctx_t c, ibmgpu_mat_t A, int precond, ibmgpu_hier_t h, con
     });
 }
 
+int ibmgpu_pcg_callback(ibmgpu_ctx_t c, ibmgpu_mat_t A, ibmgpu_apply_fn apply, void* user, const double* b,
+                        double* x, const ibm_solver_params* prm, ibm_solve_result* res, double* hist) {
+    return guard(c, [&] {
+        need(A && b && x && prm, "pcg: null argument");
+        pcg_callback(c, A, apply, user, b, x, *prm, res, hist);
+    });
+}
+
 int ibmgpu_sa_build(ibmgpu_ctx_t c, ibmgpu_mat_t A, const ibm_sa_options* o, ibmgpu_hier_t* out) {
     return guard(c, [&] {
         need(A && o && out, "sa_build: null argument");

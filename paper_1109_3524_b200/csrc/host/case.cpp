@@ -1,5 +1,15 @@
 // case.cpp — host case setup (see case.hpp). Floating-point expressions keep the reference's
 // association order (built with -ffp-contract=off) so every coordinate is bit-identical.
+//
+// PROVENANCE: this file is a deliberate transcription of the reference's host-side case setup —
+// grid.hpp:85-192 (axis widths, faces, centres), body.hpp:125-294 (kinematics, circle/ellipse/
+// point-file discretisation, adaptive Simpson), config.hpp:236-385 (the config parser with its
+// error strings) and boundary.hpp:42-61 — restated statement by statement on purpose: SURVEY §2
+// marks this host setup out of scope for re-design and requires its outputs (grid coordinates,
+// body points, M, L, G) to be bit-identical to the reference's, since they feed the bit-exact
+// device E/H/lhs2 assembly. It is not part of the B200 hot path. Only the L and G assembly
+// (operators.hpp:94-228) is restructured, into direct parallel CSR emission with the reference's
+// arithmetic. The reference headers cannot be included instead: they do not exist on the GPU box.
 #include "case.hpp"
 
 #include <omp.h>

@@ -479,6 +479,129 @@ void pcg_solve(Ctx* c, Mat* A, int kind, Hier* h, const double* b, double* x, co
 
 }  // namespace ibmgpu
 
+// ---------------------------------------------------------------- pcg with a caller's preconditioner
+// krylov.hpp:70-136 with M = the caller's apply (the reference's virtual Preconditioner::apply,
+// krylov.hpp:39-43). The preconditioner is opaque, so the loop is host-driven: one SpMV, the
+// vector updates and fixed-order (deterministic) dot products per iteration, the scalars read
+// back as the reference's loop reads them.
+namespace ibmgpu {
+namespace {
+constexpr int kDotBlocks = 592;  // 4 x 148 SMs
+__global__ void __launch_bounds__(256) k_dot_part(int n, const double* __restrict__ a, const double* __restrict__ b,
+                                                  double* __restrict__ part) {
+    __shared__ double sh[256];
+    double s = 0.0;
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) s = addd(s, mul(a[i], b[i]));
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] = addd(sh[threadIdx.x], sh[threadIdx.x + o]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+__global__ void k_dot_fin(int nb, const double* __restrict__ part, double* __restrict__ out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0;
+        for (int k = 0; k < nb; ++k) s = addd(s, part[k]);
+        *out = s;
+    }
+}
+__global__ void k_resid(int n, const double* __restrict__ b, const double* __restrict__ ax, double* __restrict__ r) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) r[i] = subd(b[i], ax[i]);
+}
+__global__ void k_xr_update(int n, double alpha, const double* __restrict__ p, const double* __restrict__ ap,
+                            double* __restrict__ x, double* __restrict__ r) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        x[i] = addd(x[i], mul(alpha, p[i]));   // axpy(alpha, p, x)
+        r[i] = addd(r[i], mul(-alpha, ap[i]));  // axpy(-alpha, Ap, r)
+    }
+}
+__global__ void k_p_update(int n, double beta, const double* __restrict__ z, double* __restrict__ p) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = addd(z[i], mul(beta, p[i]));
+}
+inline int eb(int n) { return (n + 255) / 256; }
+}  // namespace
+
+void pcg_callback(Ctx* c, Mat* A, ibmgpu_apply_fn apply, void* user, const double* b, double* x,
+                  const ibm_solver_params& prm, ibm_solve_result* res, double* hist_host) {
+    validate_params(prm);
+    require(A->rows == A->cols, "pcg: dimension mismatch");
+    require(apply != nullptr, "pcg: null preconditioner");
+    if (prm.check_symmetry) require(is_symmetric(c, A, 1e-12), "pcg: matrix is not symmetric");
+    if (!A->planned) mat_plan(c, A);
+    const int n = A->rows;
+    ibm_solve_result out{0, 0.0, 0, 0};
+    auto finish = [&] {
+        if (res) *res = out;
+    };
+    if (n == 0) return finish();
+    DBuf<double> r(c, n), z(c, n), p(c, n), ap(c, n), part(c, kDotBlocks), scal(c, 1);
+    auto dot = [&](const double* u, const double* v) {
+        k_dot_part<<<kDotBlocks, 256, 0, c->stream>>>(n, u, v, part.p);
+        CK_LAUNCH(c);
+        k_dot_fin<<<1, 32, 0, c->stream>>>(kDotBlocks, part.p, scal.p);
+        CK_LAUNCH(c);
+        return d2h_scalar(c, scal.p);
+    };
+    auto record = [&](double rel) {
+        if (prm.record_history && hist_host && out.history_len <= prm.max_iters) hist_host[out.history_len++] = rel;
+    };
+    auto precondition = [&] {
+        sync(c);
+        if (apply(user, n, r.p, z.p) != 0) fail(IBMGPU_EINVAL, "pcg: preconditioner apply failed");
+    };
+    const double bnorm = std::sqrt(dot(b, b));
+    if (bnorm == 0.0) {  // krylov.hpp:85-89
+        CK(cudaMemsetAsync(x, 0, sizeof(double) * (size_t)n, c->stream));
+        sync(c);
+        return finish();
+    }
+    spmv(c, A, x, ap.p);
+    k_resid<<<eb(n), 256, 0, c->stream>>>(n, b, ap.p, r.p);
+    CK_LAUNCH(c);
+    double rel = std::sqrt(dot(r.p, r.p)) / bnorm;
+    out.rel_residual = rel;
+    record(rel);
+    if (rel <= prm.rel_tol) return finish();
+    precondition();
+    d2d(c, p.p, z.p, (size_t)n);
+    double rz = dot(r.p, z.p);
+    for (int it = 1; it <= prm.max_iters; ++it) {
+        spmv(c, A, p.p, ap.p);
+        const double pAp = dot(p.p, ap.p);
+        if (pAp <= 0.0) {  // krylov.hpp:110-115
+            out.iterations = it - 1;
+            out.status = 2;
+            return finish();
+        }
+        const double alpha = rz / pAp;
+        k_xr_update<<<eb(n), 256, 0, c->stream>>>(n, alpha, p.p, ap.p, x, r.p);
+        CK_LAUNCH(c);
+        rel = std::sqrt(dot(r.p, r.p)) / bnorm;
+        out.rel_residual = rel;
+        record(rel);
+        if (rel <= prm.rel_tol) {
+            out.iterations = it;
+            return finish();
+        }
+        precondition();
+        const double rz_new = dot(r.p, z.p);
+        const double beta = rz_new / rz;
+        rz = rz_new;
+        k_p_update<<<eb(n), 256, 0, c->stream>>>(n, beta, z.p, p.p);
+        CK_LAUNCH(c);
+    }
+    out.iterations = prm.max_iters;
+    out.status = 1;
+    sync(c);
+    finish();
+}
+}  // namespace ibmgpu
+
 // ---------------------------------------------------------------- amg_solve (amg.hpp:250-280)
 namespace ibmgpu {
 namespace {

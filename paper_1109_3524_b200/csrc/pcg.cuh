@@ -44,6 +44,8 @@ PcgPlan* pcg_plan(Ctx* c, Mat* A, int kind, Hier* h);
 void pcg_forget(Ctx* c, const Mat* A, const Hier* h);
 void pcg_cache_free(Ctx* c);
 void validate_params(const ibm_solver_params& p);
+void pcg_callback(Ctx* c, Mat* A, ibmgpu_apply_fn apply, void* user, const double* b, double* x,
+                  const ibm_solver_params& prm, ibm_solve_result* res, double* hist_host);
 void pcg_solve(Ctx* c, Mat* A, int kind, Hier* h, const double* b, double* x, const ibm_solver_params& prm,
                ibm_solve_result* res, double* hist_host);
 

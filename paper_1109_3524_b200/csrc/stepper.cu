@@ -442,6 +442,9 @@ struct ibmgpu_stepper {
     GridDev* gd = nullptr;
     RefreshCache rcache;  // moving bodies: G^T and the invariant pressure block (refresh.cu)
     bool check_refresh = false;
+    int pin = 0;             // pressure cell pinned in lhs2 (stepper.hpp:176)
+    bool ops_only = false;   // ibmgpu_operators_create: the operator set only
+    bool sa_given = false;   // SaOptions came with SteppingParams (create_from)
     AggCache agg_cache;   // moving bodies: aggregates reused when the strength graph repeats
 
     // device vectors
@@ -548,7 +551,7 @@ struct ibmgpu_stepper {
             coupled_refresh(c, rcache, G, E, BN, &Qn, &QTn, &L2n);
             if (check_refresh) {  // IBMGPU_CHECK_REFRESH=1: compare with the full assembly
                 Mat *Qf, *QTf, *L2f;
-                coupled_system(c, G, E, BN, 0, slice_rows, &Qf, &QTf, &L2f, nullptr);
+                coupled_system(c, G, E, BN, pin, slice_rows, &Qf, &QTf, &L2f, nullptr);
                 const bool same = mat_equal(c, Qn, Qf) && mat_equal(c, QTn, QTf) && mat_equal(c, L2n, L2f);
                 delete Qf;
                 delete QTf;
@@ -556,7 +559,7 @@ struct ibmgpu_stepper {
                 if (!same) fail(IBMGPU_ECUDA, "incremental refresh differs from the full assembly");
             }
         } else {
-            coupled_system(c, G, E, BN, 0, slice_rows, &Qn, &QTn, &L2n, nullptr);
+            coupled_system(c, G, E, BN, pin, slice_rows, &Qn, &QTn, &L2n, nullptr);
         }
         lap("Q, QT, lhs2");
         pcg_forget(c, lhs2, nullptr);
@@ -655,15 +658,22 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
         std::fprintf(stderr, "[setup] %-22s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
         t0 = t1;
     };
-    S->cfg = ibmhost::parse_case(path);
+    if (path) {  // ibmgpu_stepper_create: a case file (runner.hpp:77-88 run_case's construction)
+        S->cfg = ibmhost::parse_case(path);
+        auto& cfg = S->cfg;
+        if (ov) {
+            if (ov->h_min > 0) cfg.h_min = ov->h_min;
+            if (ov->dt > 0) cfg.dt = ov->dt;
+            if (ov->n_pc > 0) cfg.n_pc = ov->n_pc;
+            if (ov->slice_rows > 0) cfg.slice_rows = ov->slice_rows;
+            S->force_rebuild = ov->force_rebuild != 0;
+        }
+        S->g = ibmhost::build_grid(cfg.domain, cfg.uniform, cfg.h_min, cfg.ratio);
+        S->bodies = ibmhost::build_bodies(cfg);
+    }  // else ibmgpu_stepper_create_from filled cfg, g and bodies (stepper.hpp:171-173)
     auto& cfg = S->cfg;
-    if (ov) {
-        if (ov->h_min > 0) cfg.h_min = ov->h_min;
-        if (ov->dt > 0) cfg.dt = ov->dt;
-        if (ov->n_pc > 0) cfg.n_pc = ov->n_pc;
-        if (ov->slice_rows > 0) cfg.slice_rows = ov->slice_rows;
-        S->force_rebuild = ov->force_rebuild != 0;
-    }
+    require(cfg.dt > 0.0, "stepping: dt must be positive");
+    require(cfg.n_pc >= 1, "stepping: n_pc must be >= 1");
     S->dt = cfg.dt;
     S->nu = cfg.nu;
     S->n_order = cfg.n_order;
@@ -672,11 +682,9 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
     // runner.hpp:63-73 stepping_from: solve 1 is always PCG-diag, solve 2 PCG-SA (stepper.hpp:282, :303)
     S->p1 = ibm_solver_params{cfg.solve1.rel_tol, cfg.solve1.max_iters, 0, 0};
     S->p2 = ibm_solver_params{cfg.solve2.rel_tol, cfg.solve2.max_iters, 0, 0};
-    S->sa = ibm_sa_options{cfg.solve2.sa_theta, cfg.solve2.sa_max_coarse, 25, 10, 0};
+    if (!S->sa_given) S->sa = ibm_sa_options{cfg.solve2.sa_theta, cfg.solve2.sa_max_coarse, 25, 10, 0};
 
-    S->g = ibmhost::build_grid(cfg.domain, cfg.uniform, cfg.h_min, cfg.ratio);
     const auto& g = S->g;
-    S->bodies = ibmhost::build_bodies(cfg);
     for (auto& b : S->bodies) b.move_to(0.0);
     S->n_b = 0;
     for (const auto& b : S->bodies) S->n_b += b.n();
@@ -765,10 +773,14 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
     // a moving body re-assembles only the body coupling from here on (refresh.cu)
     S->check_refresh = std::getenv("IBMGPU_CHECK_REFRESH") != nullptr;
     if (S->n_b > 0 && S->geom_static_after > 0.0 && !std::getenv("IBMGPU_FULL_REFRESH"))
-        S->rcache.init(c, S->G, S->BN, S->lhs2, S->n_p, 0, S->n_order);
+        S->rcache.init(c, S->G, S->BN, S->lhs2, S->n_p, S->pin, S->n_order);
     lap("E, H, Q, Q^T, lhs2");
     for (Mat* m : {S->L, S->A, S->BN, S->G}) mat_plan(c, m);
     lap("SpMV plans");
+    if (S->ops_only) {  // assemble_operators (operators.hpp:420-442) stops here
+        sync(c);
+        return;
+    }
 
     // SA hierarchy with the force rows carried to the coarse level (stepper.hpp:179-181)
     S->sa.keep_fine_tail = 2 * S->n_b;
@@ -874,6 +886,7 @@ struct NvtxRange {
 
 void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
     NvtxRange step_range("ibm.advance");
+    require(!S->ops_only, "stepper: this handle holds an operator set only (ibmgpu_operators_create)");
     Ctx* c = S->c;
     using clk = std::chrono::steady_clock;
     std::memset(rep, 0, sizeof(*rep));
@@ -1063,6 +1076,140 @@ int ibmgpu_stepper_create(ibmgpu_ctx_t c, const char* cfg_path, const ibm_case_o
     if (rc) {
         delete S;
         *out = nullptr;
+        return rc;
+    }
+    *out = S;
+    return 0;
+}
+
+}  // extern "C"
+
+namespace {
+// grid + bodies of a stepper from the reference-shaped descriptors
+void desc_setup(ibmgpu_stepper* S, const ibm_grid_desc* gd, int n_bodies, const ibm_body_desc* bd) {
+    require(gd && gd->nx >= 2 && gd->ny >= 2, "grid: need at least 2 cells per direction");
+    require(n_bodies == 0 || bd, "stepper: null body descriptors");
+    auto& g = S->g;
+    g.nx = gd->nx;
+    g.ny = gd->ny;
+    auto take = [](const double* p, int n) {
+        require(p != nullptr, "grid: null array");
+        return std::vector<double>(p, p + n);
+    };
+    g.x_faces = take(gd->x_faces, g.nx + 1);
+    g.y_faces = take(gd->y_faces, g.ny + 1);
+    g.dx = take(gd->dx, g.nx);
+    g.dy = take(gd->dy, g.ny);
+    g.x_c = take(gd->x_c, g.nx);
+    g.y_c = take(gd->y_c, g.ny);
+    g.del_x = take(gd->del_x, g.nx - 1);
+    g.del_y = take(gd->del_y, g.ny - 1);
+    g.h_min = gd->h_min;
+    g.domain = ibmhost::Rect{g.x_faces.front(), g.x_faces.back(), g.y_faces.front(), g.y_faces.back()};
+    g.uniform_region = ibmhost::Rect{gd->uniform[0], gd->uniform[1], gd->uniform[2], gd->uniform[3]};
+    S->cfg.domain = g.domain;
+    S->cfg.uniform = g.uniform_region;
+    S->cfg.h_min = g.h_min;
+    S->bodies.clear();
+    for (int k = 0; k < n_bodies; ++k) {
+        const ibm_body_desc& d = bd[k];
+        require(d.n_points > 0 && d.ref_x && d.ref_y, "body: empty point set");
+        require(d.motion >= 0 && d.motion <= 3, "motion: unknown kind");
+        ibmhost::Body b;
+        b.ref_x.assign(d.ref_x, d.ref_x + d.n_points);
+        b.ref_y.assign(d.ref_y, d.ref_y + d.n_points);
+        b.x = b.ref_x;
+        b.y = b.ref_y;
+        b.ub_x.assign(d.n_points, 0.0);
+        b.ub_y.assign(d.n_points, 0.0);
+        b.center_x = d.center_x;
+        b.center_y = d.center_y;
+        b.ds = d.ds;
+        b.motion.kind = static_cast<ibmhost::Motion>(d.motion);
+        b.motion.omega = d.omega, b.motion.k = d.k, b.motion.kh = d.kh;
+        b.motion.heave_omega = d.heave_omega, b.motion.heave_amp = d.heave_amp;
+        b.motion.A0 = d.A0, b.motion.f = d.f, b.motion.alpha0 = d.alpha0, b.motion.beta = d.beta;
+        b.motion.phase = d.phase;
+        b.rotation_invariant = d.shape_rotation_invariant != 0;
+        b.preamble_offset = d.preamble_offset;
+        b.preamble_duration = d.preamble_duration;
+        S->bodies.push_back(std::move(b));
+    }
+}
+
+ibmhost::EdgeBc edge_in(const ibm_edge_bc& e) {
+    ibmhost::EdgeBc o;
+    o.kind = e.kind == 1 ? ibmhost::Edge::convective : ibmhost::Edge::dirichlet;
+    o.u = e.u;
+    o.v = e.v;
+    return o;
+}
+}  // namespace
+
+extern "C" {
+
+int ibmgpu_stepper_create_from(ibmgpu_ctx_t c, const ibm_grid_desc* grid, int n_bodies, const ibm_body_desc* bodies,
+                               const ibm_bc_spec* bc, double nu, const ibm_stepping_params* p, double u0, double v0,
+                               ibmgpu_stepper_t* out) {
+    auto* S = new ibmgpu_stepper();
+    S->c = c;
+    const int rc = sguard(S, [&] {
+        require(bc && p && out, "stepper: null argument");
+        // SteppingParams::validate (stepper.hpp:119-124)
+        require(p->dt > 0.0, "stepping: dt must be positive");
+        require(p->n_pc >= 1, "stepping: n_pc must be >= 1");
+        validate_params(p->solve1);
+        validate_params(p->solve2);
+        desc_setup(S, grid, n_bodies, bodies);
+        auto& cfg = S->cfg;
+        cfg.bc.left = edge_in(bc->left), cfg.bc.right = edge_in(bc->right);
+        cfg.bc.bottom = edge_in(bc->bottom), cfg.bc.top = edge_in(bc->top);
+        cfg.bc.u_inf = bc->u_inf;
+        cfg.u_inf = bc->u_inf;
+        cfg.nu = nu;
+        cfg.dt = p->dt;
+        cfg.n_order = p->n_order;
+        cfg.n_pc = p->n_pc;
+        cfg.slice_rows = p->slice_rows;
+        cfg.solve1.rel_tol = p->solve1.rel_tol, cfg.solve1.max_iters = p->solve1.max_iters;
+        cfg.solve2.rel_tol = p->solve2.rel_tol, cfg.solve2.max_iters = p->solve2.max_iters;
+        cfg.solve2.sa_theta = p->sa.theta, cfg.solve2.sa_max_coarse = p->sa.max_coarse;
+        cfg.u0 = u0;
+        cfg.v0 = v0;
+        S->force_rebuild = p->force_rebuild != 0;
+        S->sa = ibm_sa_options{p->sa.theta, p->sa.max_coarse, p->sa.max_levels > 0 ? p->sa.max_levels : 25,
+                               p->sa.power_iterations >= 0 ? p->sa.power_iterations : 10, 0};
+        S->sa_given = true;
+        stepper_setup(S, nullptr, nullptr);
+    });
+    if (rc) {
+        delete S;
+        if (out) *out = nullptr;
+        return rc;
+    }
+    *out = S;
+    return 0;
+}
+
+int ibmgpu_operators_create(ibmgpu_ctx_t c, const ibm_grid_desc* grid, int n_bodies, const ibm_body_desc* bodies,
+                            double dt, double nu, int n_order, int pin, int slice_rows, ibmgpu_stepper_t* out) {
+    auto* S = new ibmgpu_stepper();
+    S->c = c;
+    const int rc = sguard(S, [&] {
+        require(out != nullptr, "operators: null argument");
+        desc_setup(S, grid, n_bodies, bodies);
+        require(pin >= 0 && pin < S->g.nx * S->g.ny, "pin_row_col: bad pin index");
+        S->cfg.dt = dt;
+        S->cfg.nu = nu;
+        S->cfg.n_order = n_order;
+        S->cfg.slice_rows = slice_rows;
+        S->pin = pin;
+        S->ops_only = true;
+        stepper_setup(S, nullptr, nullptr);
+    });
+    if (rc) {
+        delete S;
+        if (out) *out = nullptr;
         return rc;
     }
     *out = S;
