@@ -771,6 +771,19 @@ struct StepReport {
     double solve1_res = 0, solve2_res = 0, div_residual = 0, noslip_residual = 0;
     bool rebuilt_hierarchy = false, rebuilt_operators = false;
     double bc_cfl = 0, t_assembly = 0, t_precond = 0, t_explicit = 0, t_solve1 = 0, t_solve2 = 0, t_projection = 0;
+    // converts to the reference's own StepReport (same members), so code written against
+    // ibm::StepReport (`StepReport rep = st.advance();` in runner.hpp:102) keeps compiling
+    template <class T, class = decltype(std::declval<T&>().t_projection), class = decltype(std::declval<T&>().message)>
+    operator T() const {
+        T t;
+        t.ok = ok, t.message = message, t.solve1_iters = solve1_iters, t.solve2_iters = solve2_iters;
+        t.solve1_res = solve1_res, t.solve2_res = solve2_res, t.div_residual = div_residual;
+        t.noslip_residual = noslip_residual, t.rebuilt_hierarchy = rebuilt_hierarchy;
+        t.rebuilt_operators = rebuilt_operators, t.bc_cfl = bc_cfl, t.t_assembly = t_assembly;
+        t.t_precond = t_precond, t.t_explicit = t_explicit, t.t_solve1 = t_solve1, t.t_solve2 = t_solve2;
+        t.t_projection = t_projection;
+        return t;
+    }
 };
 struct FlowState {
     std::vector<double> q, conv_prev, phi, f_tilde, lambda;
@@ -794,6 +807,51 @@ public:
         ibmgpu_stepper_t s = nullptr;
         check(ibmgpu_stepper_create_from(Context::get().h(), &gd, (int)bd.size(), bd.data(), &bs, nu, &sp, u0, v0, &s));
         init(s, grid, params.dt, nu, params.n_order, params.slice_rows, bc.u_inf);
+    }
+    // The same constructor taking the REFERENCE's own objects (ibm::StaggeredGrid, ibm::LagrangianBody,
+    // ibm::BcSpec, ibm::SteppingParams — any types with the reference's member names): the
+    // reference's run_case (runner.hpp:86-88) switches to the device path by changing only the
+    // declared type of `st` (INTEGRATION.md shows the diff; oracle/Makefile builds it).
+    template <class Grid, class Body, class Bc, class Params>
+    Stepper(const Grid& grid, const std::vector<Body>& bodies, const Bc& bc, double nu, const Params& params,
+            double u0 = 0.0, double v0 = 0.0) {
+        StaggeredGrid g;
+        g.nx = grid.nx, g.ny = grid.ny;
+        g.x_faces = grid.x_faces, g.y_faces = grid.y_faces, g.dx = grid.dx, g.dy = grid.dy;
+        g.x_c = grid.x_c, g.y_c = grid.y_c, g.del_x = grid.del_x, g.del_y = grid.del_y;
+        g.domain = Rect{grid.domain.x0, grid.domain.x1, grid.domain.y0, grid.domain.y1};
+        g.uniform_region = Rect{grid.uniform_region.x0, grid.uniform_region.x1, grid.uniform_region.y0,
+                                grid.uniform_region.y1};
+        g.h_min = grid.h_min;
+        std::vector<LagrangianBody> bs;
+        for (const auto& b : bodies) {
+            LagrangianBody o;
+            o.ref_x = b.ref_x, o.ref_y = b.ref_y, o.x = b.x, o.y = b.y, o.ub_x = b.ub_x, o.ub_y = b.ub_y;
+            o.center_x = b.center_x, o.center_y = b.center_y, o.ds = b.ds;
+            const auto& m = b.motion;
+            o.motion = MotionParams{static_cast<MotionKind>(static_cast<int>(m.kind)), m.omega, m.k, m.kh,
+                                    m.heave_omega, m.heave_amp, m.A0, m.f, m.alpha0, m.beta, m.phase};
+            o.shape_rotation_invariant = b.shape_rotation_invariant;
+            o.preamble_offset = b.preamble_offset, o.preamble_duration = b.preamble_duration;
+            bs.push_back(std::move(o));
+        }
+        auto edge = [](const auto& e) {
+            return EdgeBc{static_cast<int>(e.kind) == 1 ? BcKind::convective : BcKind::dirichlet, e.u, e.v};
+        };
+        const BcSpec b2{edge(bc.left), edge(bc.right), edge(bc.bottom), edge(bc.top), bc.u_inf};
+        SteppingParams p;
+        p.dt = params.dt, p.n_order = params.n_order, p.n_pc = params.n_pc;
+        p.force_rebuild = params.force_rebuild, p.slice_rows = params.slice_rows;
+        auto sp = [](const auto& s) {
+            SolverParams r;
+            r.rel_tol = s.rel_tol, r.max_iters = s.max_iters;
+            r.record_history = s.record_history, r.check_symmetry = s.check_symmetry;
+            return r;
+        };
+        p.solve1 = sp(params.solve1), p.solve2 = sp(params.solve2);
+        p.sa = SaOptions{params.sa.theta, params.sa.max_coarse, params.sa.max_levels, params.sa.power_iterations,
+                         params.sa.keep_fine_tail};
+        *this = Stepper(g, std::move(bs), b2, nu, p, u0, v0);
     }
     // from a case file (what run_case constructs, runner.hpp:77-88)
     explicit Stepper(const std::string& cfg_path, const ibm_case_overrides& ov = ibm_case_overrides{}) {
@@ -863,6 +921,26 @@ public:
         return hier_;
     }
     const StaggeredGrid& grid() const { return grid_; }
+    // BoundaryState (boundary.hpp:34-40): the stored edge values in the reference's layout, as
+    // any struct with its member names (e.g. ibm::BoundaryState for couette_profile_error)
+    template <class BS>
+    BS boundary_as() const {
+        const auto v = get(3);
+        const auto [nx, ny] = grid_dims();
+        BS out;
+        size_t o = 0;
+        auto take = [&](std::vector<double>& dst, int n) {
+            dst.assign(v.begin() + (long)o, v.begin() + (long)o + n);
+            o += (size_t)n;
+        };
+        take(out.left_u, ny), take(out.right_u, ny), take(out.left_v, ny - 1), take(out.right_v, ny - 1);
+        take(out.bottom_v, nx), take(out.top_v, nx), take(out.bottom_u, nx - 1), take(out.top_u, nx - 1);
+        return out;
+    }
+    struct BoundaryState {
+        std::vector<double> left_u, right_u, left_v, right_v, bottom_v, top_v, bottom_u, top_u;
+    };
+    BoundaryState boundary() const { return boundary_as<BoundaryState>(); }
     // compute_force_coefficients on the device copy of f~ (diagnostics.hpp:26-38): {fx, fy, cd, cl}
     std::vector<double> forces() const {
         std::vector<double> f(4);
