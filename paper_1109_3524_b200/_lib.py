@@ -54,6 +54,29 @@ class CaseOverridesC(C.Structure):
                 ("slice_rows", C.c_int)]
 
 
+class EdgeBcC(C.Structure):
+    _fields_ = [("kind", C.c_int), ("u", C.c_double), ("v", C.c_double)]
+
+
+class BcSpecC(C.Structure):
+    _fields_ = [("left", EdgeBcC), ("right", EdgeBcC), ("bottom", EdgeBcC), ("top", EdgeBcC), ("u_inf", C.c_double)]
+
+
+class SolverConfigC(C.Structure):
+    _fields_ = [("kind", C.c_int), ("rel_tol", C.c_double), ("max_iters", C.c_int), ("sa_theta", C.c_double),
+                ("sa_max_coarse", C.c_int)]
+
+
+class CaseConfigC(C.Structure):
+    """ibm_case_config: the scalar part of CaseConfig (config.hpp:54-95) from the native parser."""
+    _fields_ = [("domain", C.c_double * 4), ("uniform", C.c_double * 4), ("h_min", C.c_double),
+                ("ratio", C.c_double * 4), ("nu", C.c_double), ("re", C.c_double), ("u_inf", C.c_double),
+                ("ref_length", C.c_double), ("u0", C.c_double), ("v0", C.c_double), ("dt", C.c_double),
+                ("n_steps", C.c_int), ("n_out", C.c_int), ("checkpoint_every", C.c_int), ("n_pc", C.c_int),
+                ("n_order", C.c_int), ("slice_rows", C.c_int), ("n_bodies", C.c_int), ("bc", BcSpecC),
+                ("solve1", SolverConfigC), ("solve2", SolverConfigC), ("out_dir", C.c_char * 512)]
+
+
 class StepReportC(C.Structure):
     _fields_ = [("ok", C.c_int), ("solve1_iters", C.c_int), ("solve2_iters", C.c_int), ("solve1_res", C.c_double),
                 ("solve2_res", C.c_double), ("div_residual", C.c_double), ("noslip_residual", C.c_double),
@@ -126,6 +149,7 @@ _SIGS = [
     ("ibmgpu_hostcase_csr", C.c_int, [_vp, C.c_char_p, _ip, _ip, _ip, _ip, _ip, _dp]),
     ("ibmgpu_hostcase_move", C.c_int, [_vp, C.c_double]),
     ("ibmgpu_hostcase_free", C.c_int, [_vp]),
+    ("ibmgpu_host_case_config", C.c_int, [C.c_char_p, C.POINTER(CaseConfigC), C.c_char_p, C.c_int]),
     ("ibmgpu_nccl_unique_id", C.c_int, [_vp]),
     ("ibmgpu_dist_create", C.c_int, [_vp, _vp, C.c_int, _vp, _ip, C.c_int, C.c_int, C.POINTER(_vp)]),
     ("ibmgpu_dist_info", C.c_int, [_vp, _ip]),

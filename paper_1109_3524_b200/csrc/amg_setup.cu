@@ -1023,6 +1023,7 @@ struct AuxStream {
         c.device = main->device;
         c.num_sms = main->num_sms;
         c.eager = main->eager;
+        c.pool = main->pool;
         CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));

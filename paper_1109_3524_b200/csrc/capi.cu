@@ -1,6 +1,7 @@
 // capi.cu — extern "C" entry points of include/ibmgpu.h (context, memory, CSR, solvers).
 // Every call is wrapped so that C++ exceptions become IBMGPU_E* codes + ibmgpu_last_error().
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 
@@ -59,28 +60,33 @@ int ibmgpu_init(int device, int nranks, int rank, const void* nccl_id, ibmgpu_ct
         CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
         const char* eg = std::getenv("IBMGPU_EAGER");
         c->eager = eg && eg[0] == '1';
-        cudaMemPool_t pool;
-        CK(cudaDeviceGetDefaultMemPool(&pool, device));
-        unsigned long long thr = ~0ull;  // keep freed blocks cached in the pool
-        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-        // Pre-map part of the pool once per device: the SpGEMM sort buffers of a hierarchy rebuild
-        // (up to ~2 GB at 600k rows) otherwise map fresh pages mid-setup, which made identical
-        // rebuilds vary 65-500 ms (IBMGPU_POOL_RESERVE_MB, default 8192; 0 disables).
-        static bool reserved[64] = {};
+        // A private stream-ordered pool: freed blocks stay cached for the context's own reuse, and
+        // nothing process-wide (the device's default pool, other allocators) is touched.
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        CK(cudaMemPoolCreate(&c->pool, &props));
+        unsigned long long thr = ~0ull;  // keep freed blocks cached in this pool
+        CK(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        // Pre-map part of the pool for the first context on a device: the SpGEMM sort buffers of
+        // a hierarchy rebuild (up to ~2 GB at 600k rows) otherwise map fresh pages mid-setup,
+        // which made identical rebuilds vary 65-500 ms (IBMGPU_POOL_RESERVE_MB, default 8192;
+        // 0 disables). The once-per-device claim is an atomic exchange (thread-safe).
+        static std::atomic<bool> reserved[64] = {};
         const char* rv = std::getenv("IBMGPU_POOL_RESERVE_MB");
         const size_t mb = rv ? std::strtoull(rv, nullptr, 10) : 8192;
-        if (mb && device >= 0 && device < 64 && !reserved[device]) {
+        if (mb && device >= 0 && device < 64 && !reserved[device].exchange(true)) {
             size_t free_b = 0, total_b = 0;
             CK(cudaMemGetInfo(&free_b, &total_b));
             const size_t want = std::min(mb << 20, free_b / 4);
             void* p = nullptr;
-            if (cudaMallocAsync(&p, want, c->stream) == cudaSuccess) {
+            if (cudaMallocFromPoolAsync(&p, want, c->pool, c->stream) == cudaSuccess) {
                 CK(cudaFreeAsync(p, c->stream));
                 CK(cudaStreamSynchronize(c->stream));
             } else {
                 cudaGetLastError();
             }
-            reserved[device] = true;
         }
         need(nranks == 1 || nccl_id != nullptr, "init: multi-rank context needs an NCCL unique id");
         // nranks == 1 with an id: a one-rank NCCL communicator (exercises the NCCL code path)
@@ -104,6 +110,7 @@ int ibmgpu_destroy(ibmgpu_ctx_t c) {
     cudaEventDestroy(c->t0);
     cudaEventDestroy(c->t1);
     cudaStreamDestroy(c->stream);
+    if (c->pool) cudaMemPoolDestroy(c->pool);  // released once its last allocation is freed
     delete c;
     return 0;
 }
@@ -116,7 +123,7 @@ int ibmgpu_synchronize(ibmgpu_ctx_t c) {
 
 int ibmgpu_vec_alloc(ibmgpu_ctx_t c, size_t n, double** dev) {
     return guard(c, [&] {
-        CK(cudaMallocAsync(reinterpret_cast<void**>(dev), sizeof(double) * (n ? n : 1), c->stream));
+        CK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(dev), sizeof(double) * (n ? n : 1), c->pool, c->stream));
         CK(cudaMemsetAsync(*dev, 0, sizeof(double) * (n ? n : 1), c->stream));
     });
 }

@@ -423,10 +423,12 @@ void exchange(Dist* d, GetM gm, GetV gv) {
     }
     if (d->R == 1) return;
     if (d->loop) {
-        // IBMGPU_DIST_NOCOPY=1 (timing experiments only, results are wrong): skip the loopback halo
-        // copies to separate their cost from the ranks' own work
+#ifdef IBMGPU_TIMING_EXPERIMENTS
+        // IBMGPU_DIST_NOCOPY=1 (timing builds only, results are wrong): skip the loopback halo
+        // copies to separate their cost from the ranks' own work. Never compiled into the product.
         static const bool nocopy = std::getenv("IBMGPU_DIST_NOCOPY") != nullptr;
         if (nocopy) return;
+#endif
         if (d->loop_nccl) {
             // every virtual rank's halo through the NCCL p2p path: send/recv pairs to self, issued
             // in the same order so the k-th send matches the k-th receive

@@ -57,6 +57,7 @@ struct ibmgpu_ctx {
     void* pcg_cache = nullptr;  // pcg.cu plan cache
     int eager = 0;              // IBMGPU_EAGER=1: host-looped solves (profiling only)
     int pdl_fence = 0;          // set by plain launches: the next launch_k skips PDL (CK_LAUNCH)
+    cudaMemPool_t pool = nullptr;  // the context's own stream-ordered pool (capi.cu ibmgpu_init)
 };
 
 namespace ibmgpu {
@@ -87,7 +88,12 @@ struct DBuf {
         release();
         s = c->stream;
         n = count;
-        if (count) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, s));
+        if (count) {
+            if (c->pool)
+                CK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, c->pool, s));
+            else
+                CK(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, s));
+        }
     }
     void release() {
         if (p) cudaFreeAsync(p, s);

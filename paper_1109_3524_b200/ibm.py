@@ -820,22 +820,17 @@ class DistSolver:
 
 
 # ----------------------------------------------------------------------------- run loop (runner.hpp)
-def _cfg_values(cfg_path: str) -> dict:
-    """The run-loop keys of a case file ([time] n_steps/n_out, [output] dir/checkpoint_every);
-    everything else is parsed by the native case loader."""
-    vals, sec = {}, ""
-    with open(cfg_path) as f:
-        for raw in f:
-            line = raw.split("#", 1)[0].strip()
-            if not line:
-                continue
-            if line.startswith("["):
-                sec = line.strip("[]").strip()
-                continue
-            if "=" in line:
-                k, v = (x.strip() for x in line.split("=", 1))
-                vals[f"{sec}.{k}"] = v
-    return vals
+def case_config(cfg_path: str):
+    """parse_config (config.hpp:236-355) by the library's native parser: the scalar CaseConfig
+    fields (n_steps, n_out, out_dir, checkpoint_every, ...) exactly as the reference reads them."""
+    from ._lib import IBMGPU_EINVAL, CaseConfigC
+    cfg = CaseConfigC()
+    err = C.create_string_buffer(512)
+    rc = load().ibmgpu_host_case_config(cfg_path.encode(), C.byref(cfg), err, 512)
+    if rc:
+        msg = err.value.decode(errors="replace")
+        raise ValueError(msg) if rc == IBMGPU_EINVAL else RuntimeError(msg)
+    return cfg
 
 
 @dataclass
@@ -861,12 +856,12 @@ def run_case(cfg_path: str, out_dir: str | None = None, n_steps: int = 0, resume
     ("x y omega", %.9g), checkpoint_<k>.txt every checkpoint_every steps and checkpoint_final.txt
     (io.hpp format)."""
     import os
-    v = _cfg_values(cfg_path)
-    out = out_dir or v.get("output.dir", "out")
+    cfg = case_config(cfg_path)
+    out = out_dir or cfg.out_dir.decode()
     os.makedirs(out, exist_ok=True)
-    n_total = n_steps or int(v.get("time.n_steps", "0"))
-    n_out = int(v.get("time.n_out", "0"))
-    ckpt_every = int(v.get("output.checkpoint_every", "0"))
+    n_total = n_steps or cfg.n_steps
+    n_out = cfg.n_out
+    ckpt_every = cfg.checkpoint_every
     st = Stepper(cfg_path, **stepper_kw)
     if resume_from:
         st.read_checkpoint(resume_from)
