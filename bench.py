@@ -8,13 +8,16 @@ N > 1 (torchrun, one process per GPU): the coupled solve runs row-slab distribut
 
 A "step" is one Stepper::advance (stepper.hpp:231-356): explicit terms, PCG-diag momentum solve,
 SA-PCG coupled solve, projection and invariants, all resident in HBM (device-built operators and
-SA hierarchy). Prints ONE JSON line (rank 0). Default workload: C2 = impulsively started cylinder,
-Re 40, ~1M cells (cylinder_re40.cfg at h_min 0.002 -> 1042^2), BASELINE.json configs[1]; the
-S-4M (configs[2]) per-iteration roofline is reported alongside under "s4m" unless --no-s4m, and
-the moving-body case (configs[3]) under "flapping" unless --no-flapping.
+SA hierarchy). Prints ONE JSON line (rank 0). Default workload: S-4M = the north-star case,
+impulsively started cylinder at ~4M cells (cylinder_re3000.cfg geometry at h_min 0.001 ->
+2040^2, BASELINE.json configs[2]). Alongside: C2 (configs[1], 1042^2) under "c2", the
+moving-body case (configs[3]) under "flapping", the synthetic C5 grids 1024^2..8192^2
+(configs[4]) under "grid_sweep", and the reference CPU Stepper under "cpu_baseline".
 
 --impl reference runs the reference's own CPU implementation (oracle/_ref/libibmref.so, the
 unmodified reference headers) on the same case with all host threads; it never touches the GPU.
+Its steps are a bounded sample (at most --ref-warmup / --ref-steps steps, default 1 / 2) so the
+run ends within minutes at S-4M, where one reference step takes ~30 s on 16 cores.
 """
 from __future__ import annotations
 
@@ -34,11 +37,20 @@ CASES = os.path.join(ROOT, "cases")
 WORKLOADS = {
     # name: (cfg, h_min override, dt override, description)
     "c2": ("cylinder_re40", 0.002, 0.001, "Re40 impulsively started cylinder, h_min 0.002 (1042^2, ~1.09M-row lhs2)"),
-    "s4m": ("cylinder_re3000", 0.001, 2.5e-4, "Re3000 cylinder geometry, h_min 0.001 (2040^2, 4.17M-row lhs2)"),
+    # dt 1.25e-4 (CFL 0.125): at SURVEY's dt 2.5e-4 this case blows up in the reference itself (max |q|
+    # 0.198 / 3.76 / 1006 at steps 4 / 5 / 6, identical on the device; tools/diag/ref_s4m_growth.py)
+    "s4m": ("cylinder_re3000", 0.001, 1.25e-4, "Re3000 impulsively started cylinder, h_min 0.001 (2040^2, "
+                                               "4.17M-row lhs2), dt 1.25e-4"),
     "c2a": ("cylinder_re40", 0.0, 0.0, "Re40 cylinder 330^2 (reference cfg)"),
     "cavity": ("cavity", 0.0, 0.0, "lid-driven cavity Re100 128^2, no body"),
     "flapping": ("flapping", 0.0, 0.0, "flapping ellipse 930x654, moving body (lhs2 rebuilt every step)"),
 }
+
+
+def config_of(name: str) -> dict:
+    """The `config` object of both arms (identical keys and values, so the lines compare)."""
+    cfg, h_min, dt, desc = workload(name)
+    return {"workload": name, "case": cfg + ".cfg", "h_min": h_min or None, "dt": dt or None, "desc": desc}
 
 
 def workload(name: str):
@@ -125,11 +137,15 @@ def hier_bytes(h) -> tuple[float, dict]:
 def load_traffic(workload: str):
     """Measured DRAM bytes per solve-2 iteration from the committed ncu launch list
     (profiles/r01/traffic.json, tools/traffic_per_iteration.py); None if not captured."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "traffic.json")) as f:
-            return json.load(f).get(workload)
-    except Exception:
-        return None
+    for rnd in ("r02", "r01"):  # newest capture first
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "traffic.json")) as f:
+                d = json.load(f).get(workload)
+            if d:
+                return d
+        except Exception:
+            continue
+    return None
 
 
 def load_peaks():
@@ -239,14 +255,14 @@ def run_ours(args, rank: int, world: int):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (deterministic case file; no datasets)",
-        "config": {"workload": args.workload, "case": cfg + ".cfg", "h_min": h_min or None, "dt": dt or None,
-                   "desc": desc, "grid": [st.nx, st.ny], "n_lambda": st.n_lambda, "nnz_lhs2": st.nnz_lhs2,
-                   "n_b": n_b, "sa_levels": len(hinfo["levels"]), "n_c": hinfo["n_c"],
-                   "parallelism": (f"row-slab x{world} (solve 2 distributed over NCCL, min_dist_rows "
-                                   f"{args.min_dist_rows}; explicit terms + solve 1 replicated)") if slab else
-                                  ("replicas" if world > 1 else "single-gpu"),
-                   "l2": "inputs larger than L2 (per-iteration working set >> 126 MB)" if b_it2 > 5e8 else
-                   "working set partly L2-resident"},
+        "config": config_of(args.workload),
+        "parallelism": (f"row-slab x{world} (solve 2 distributed over NCCL, min_dist_rows "
+                        f"{args.min_dist_rows}; explicit terms + solve 1 replicated)") if slab else
+                       ("replicas" if world > 1 else "single-gpu"),
+        "l2": "inputs larger than L2 (per-iteration working set >> 126 MB)" if b_it2 > 5e8 else
+              "working set partly L2-resident",
+        "problem": {"grid": [st.nx, st.ny], "n_lambda": st.n_lambda, "nnz_lhs2": st.nnz_lhs2, "n_b": n_b,
+                    "sa_levels": len(hinfo["levels"]), "n_c": hinfo["n_c"]},
         "cg_iters_per_step": round(sum(its2) / K, 2),
         "momentum_iters_per_step": round(sum(its1) / K, 2),
         "cg_iters_per_s": round(sum(its2) / (sum(solve2_ms) * 1e-3), 1),
@@ -268,18 +284,19 @@ def run_ours(args, rank: int, world: int):
     return out, st
 
 
-def s4m_probe(args) -> dict:
-    """S-4M per-iteration roofline (north-star target: >= 60% of HBM roofline per CG iteration)."""
+def case_probe(args, name: str) -> dict:
+    """Steps/s and the per-CG-iteration roofline of another cylinder workload (device-timed phases)."""
     from paper_1109_3524_b200 import ibm
-    cfg, h_min, dt, desc = WORKLOADS["s4m"]
+    cfg, h_min, dt, desc = WORKLOADS[name]
     t0 = time.time()
     st = ibm.Stepper(os.path.join(CASES, cfg + ".cfg"), h_min=h_min, dt=dt)
     setup = time.time() - t0
     b_it2, hinfo = hier_bytes(st.hierarchy())
-    st.advance()
+    for _ in range(3):
+        st.advance()
     ms, its = [], []
     step_ms = []
-    for _ in range(max(2, min(args.steps, 5))):
+    for _ in range(max(3, min(args.steps, 10))):
         r = st.advance()
         ph = st.phase_ms()
         ms.append(ph["solve2"])
@@ -288,7 +305,7 @@ def s4m_probe(args) -> dict:
     peak, kind = load_peaks()
     it_ms = sum(ms) / sum(its)
     ach = b_it2 / (it_ms * 1e-3) / 1e9
-    return {"grid": [st.nx, st.ny], "n_lambda": st.n_lambda, "setup_s": round(setup, 2),
+    return {"config": config_of(name), "grid": [st.nx, st.ny], "n_lambda": st.n_lambda, "setup_s": round(setup, 2),
             "cg_iters_per_step": sum(its) / len(its), "cg_iteration_ms": round(it_ms, 4),
             "b_it2_gb": round(b_it2 / 1e9, 3), "achieved_gbs": round(ach, 1), "frac_measured": round(ach / peak, 4),
             "frac_of_8tbs": round(ach / 8000, 4), "steps_per_s": round(1e3 / (sum(step_ms) / len(step_ms)), 3),
@@ -317,8 +334,26 @@ def flapping_probe(args) -> dict:
             "cg_iters_per_step": sum(r.solve2_iters for r in reps) / n}
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def ref_phase_seconds(reports) -> dict:
+    """The reference's own per-phase timing (StepReport, stepper.hpp:139-144; runner.hpp:18-42)."""
+    keys = ("t_assembly", "t_precond", "t_explicit", "t_solve1", "t_solve2", "t_projection")
+    return {k[2:]: round(sum(r[k] for r in reports) / len(reports), 4) for k in keys}
+
+
 def cpu_baseline(args) -> dict:
-    """Reference CPU path (oracle/_ref) on a bounded sample of the same workload (rank 0 only)."""
+    """Reference CPU path (oracle/_ref) on a bounded sample of the same workload (rank 0 only):
+    --cpu-steps timed steps after one warm-up step, all host threads."""
     from oracle import oracle as O
     cfg, h_min, dt, _ = workload(args.workload)
     R = O.ref()
@@ -330,12 +365,33 @@ def cpu_baseline(args) -> dict:
     n = args.cpu_steps
     c.step()  # first step (forward Euler bootstrap) excluded
     t1 = time.time()
-    for _ in range(n):
-        c.step()
+    reps = [c.step() for _ in range(n)]
     el = time.time() - t1
     return {"value": round(n / el, 5), "unit": "steps/s", "cores": cores, "kind": "reference",
-            "sample": f"{n} Stepper::advance steps of {args.workload} after 1 warm-up step "
+            "cpu_model": cpu_model(), "setup_s": round(setup, 1), "phase_s": ref_phase_seconds(reps),
+            "sample": f"{n} Stepper::advance step(s) of {args.workload} after 1 warm-up step "
                       f"(setup {setup:.1f}s excluded), OMP_NUM_THREADS={cores}"}
+
+
+def cpu_threads_figure(name: str = "c2") -> dict:
+    """The reference Stepper on C2 with all host threads and with one thread (one step each after a
+    warm-up step): the CPU model's scaling, next to the all-core figure of the headline case."""
+    from oracle import oracle as O
+    cfg, h_min, dt, _ = workload(name)
+    R = O.ref()
+    cores = os.cpu_count() or 1
+    R.set_threads(cores)
+    c = R.case(os.path.join(CASES, cfg + ".cfg"), h_min, dt)
+    c.step()
+    out = {"config": config_of(name), "cpu_model": cpu_model(), "unit": "steps/s"}
+    for threads in (cores, 1):
+        R.set_threads(threads)
+        t1 = time.time()
+        rep = c.step()
+        el = time.time() - t1
+        out[f"threads_{threads}"] = {"value": round(1 / el, 5), "phase_s": ref_phase_seconds([rep])}
+    R.set_threads(cores)
+    return out
 
 
 def run_reference(args):
@@ -350,23 +406,26 @@ def run_reference(args):
     t0 = time.time()
     c = R.case(os.path.join(CASES, cfg + ".cfg"), h_min, dt)
     setup = time.time() - t0
-    for _ in range(args.warmup):
+    # bounded sample: at most --ref-warmup / --ref-steps steps (a reference S-4M step is ~30 s)
+    W = min(args.warmup, args.ref_warmup)
+    K = max(1, min(args.steps, args.ref_steps))
+    for _ in range(W):
         c.step()
     t1 = time.time()
-    its = 0
-    for _ in range(args.steps):
-        its += c.step()["solve2_iters"]
+    reps = [c.step() for _ in range(K)]
     el = time.time() - t1
-    v = args.steps / el
+    its = sum(r["solve2_iters"] for r in reps)
+    v = K / el
+    sample = (f"{K} timed Stepper::advance step(s) after {W} warm-up (bounded sample of the requested "
+              f"--steps {args.steps} --warmup {args.warmup}; setup {setup:.1f}s excluded), OMP_NUM_THREADS={cores}")
     return {"impl": "reference", "metric": "time steps/sec (IBPM step: explicit + PCG-diag + SA-PCG + projection)",
-            "value": round(v, 5), "unit": "steps/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "value": round(v, 5), "unit": "steps/s", "n_gpus": 1, "steps": K, "warmup": W,
+            "ms_per_step": round(el / K * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic case file)",
-            "config": {"workload": args.workload, "case": cfg + ".cfg", "h_min": h_min or None, "dt": dt or None,
-                       "desc": desc},
-            "cg_iters_per_step": its / args.steps, "setup_s": round(setup, 2),
+            "config": config_of(args.workload), "parallelism": f"host OpenMP x{cores}",
+            "cg_iters_per_step": its / K, "setup_s": round(setup, 2), "phase_s": ref_phase_seconds(reps),
             "cpu_baseline": {"value": round(v, 5), "unit": "steps/s", "cores": cores, "kind": "reference",
-                             "sample": f"{args.steps} timed Stepper::advance steps after {args.warmup} warm-up"},
+                             "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": round(v, 5), "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -375,13 +434,16 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--workload", default="s4m")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--cpu-steps", type=int, default=1)
+    ap.add_argument("--ref-steps", type=int, default=2, help="--impl reference: at most this many timed steps")
+    ap.add_argument("--ref-warmup", type=int, default=1, help="--impl reference: at most this many warm-up steps")
+    ap.add_argument("--no-cpu-threads", action="store_true", help="skip the C2 all-core / 1-thread CPU figure")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-s4m", action="store_true")
+    ap.add_argument("--no-s4m", action="store_true", help="skip the S-4M / C2 side probe")
     ap.add_argument("--no-flapping", action="store_true")
-    ap.add_argument("--no-sweep", action="store_true", help="skip the C5 grid-size sweep (1024^2..4096^2)")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C5 grid-size sweep (1024^2..8192^2)")
     ap.add_argument("--parallel", default="slab", choices=["slab", "replicas"],
                     help="N>1: row-slab distributed solve 2 over NCCL (one simulation), or N replicas")
     ap.add_argument("--min-dist-rows", type=int, default=200000,
@@ -419,23 +481,26 @@ def main():
         dist.barrier()
     if rank == 0:
         del st
-        if not args.no_s4m and args.workload != "s4m" and world == 1:
-            try:
-                out["s4m"] = s4m_probe(args)
-            except Exception as e:  # report, never hide
-                out["s4m"] = {"error": str(e)}
+        if not args.no_s4m and world == 1:  # the other cylinder workload of the pair C2 / S-4M
+            side = "c2" if args.workload == "s4m" else "s4m"
+            if args.workload in ("s4m", "c2"):
+                try:
+                    out[side] = case_probe(args, side)
+                except Exception as e:  # report, never hide
+                    out[side] = {"error": str(e)}
         if not args.no_flapping and args.workload != "flapping" and world == 1:
             try:
                 out["flapping"] = flapping_probe(args)
             except Exception as e:
                 out["flapping"] = {"error": str(e)}
-        if not args.no_sweep and world == 1 and args.workload == "c2":
+        if not args.no_sweep and world == 1 and args.workload in ("s4m", "c2"):
             try:  # BASELINE metric "CG iters/sec vs grid size" (configs[4] synthetic grids)
                 sys.path.insert(0, os.path.join(ROOT, "tools"))
                 import sweep as _sweep
-                out["grid_sweep"] = [{k: r[k] for k in ("grid", "cg_iters_per_s", "cg_iteration_ms", "cg_frac_measured",
-                                                        "spmv_hbm_gbs", "steps_per_s")}
-                                     for r in _sweep.sweep([1024, 2048, 4096], spmv_reps=10)]
+                keys = ("grid", "setup_s", "cg_iters_per_s", "cg_iteration_ms", "cg_frac_measured", "spmv_lhs2_us",
+                        "spmv_format_gbs", "spmv_format_frac_measured", "steps_per_s")
+                out["grid_sweep"] = [{k: r[k] for k in keys}
+                                     for r in _sweep.sweep([1024, 2048, 4096, 8192], spmv_reps=10)]
             except Exception as e:
                 out["grid_sweep"] = {"error": str(e)}
         if not args.no_cpu and world == 1:
@@ -443,6 +508,11 @@ def main():
                 out["cpu_baseline"] = cpu_baseline(args)
             except Exception as e:
                 out["cpu_baseline"] = {"error": str(e)}
+            if not args.no_cpu_threads:
+                try:
+                    out["cpu_threads"] = cpu_threads_figure("c2")
+                except Exception as e:
+                    out["cpu_threads"] = {"error": str(e)}
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist

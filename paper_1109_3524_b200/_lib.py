@@ -150,6 +150,7 @@ _SIGS = [
     ("ibmgpu_hostcase_move", C.c_int, [_vp, C.c_double]),
     ("ibmgpu_hostcase_free", C.c_int, [_vp]),
     ("ibmgpu_host_case_config", C.c_int, [C.c_char_p, C.POINTER(CaseConfigC), C.c_char_p, C.c_int]),
+    ("ibmgpu_csr_format_bytes", C.c_int, [_vp, _vp, C.POINTER(C.c_longlong), _ip]),
     ("ibmgpu_nccl_unique_id", C.c_int, [_vp]),
     ("ibmgpu_dist_create", C.c_int, [_vp, _vp, C.c_int, _vp, _ip, C.c_int, C.c_int, C.POINTER(_vp)]),
     ("ibmgpu_dist_info", C.c_int, [_vp, _ip]),

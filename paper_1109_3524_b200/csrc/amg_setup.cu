@@ -1067,10 +1067,15 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o, AggCache* cac
             CK(cudaEventRecord(aux.fork, c->stream));
             CK(cudaStreamWaitEvent(aux.c.stream, aux.fork, 0));
             const double* invd_p = L->invd.p;
-            auto rho_f = std::async(std::launch::async, [&aux, A, invd_p, &o, dev = c->device] {
-                CK(cudaSetDevice(dev));
-                return rho_dinv_a(&aux.c, A, invd_p, o.power_iterations);
-            });
+            static const bool aux_on = [] {
+                const char* e = std::getenv("IBMGPU_AUX");  // IBMGPU_AUX=0: power iteration inline
+                return !(e && e[0] == '0');
+            }();
+            auto rho_f = std::async(aux_on ? std::launch::async : std::launch::deferred,
+                                    [&aux, A, invd_p, &o, dev = c->device] {
+                                        CK(cudaSetDevice(dev));
+                                        return rho_dinv_a(&aux.c, A, invd_p, o.power_iterations);
+                                    });
             bool hit = false;
             int n_agg = 0;
             try {

@@ -189,6 +189,32 @@ int ibmgpu_csr_info(ibmgpu_mat_t m, int* rows, int* cols, int* nnz) {
     return 0;
 }
 
+int ibmgpu_csr_format_bytes(ibmgpu_ctx_t c, ibmgpu_mat_t m, long long* bytes, int* kind) {
+    return guard(c, [&] {
+        need(m && bytes, "csr_format_bytes: null argument");
+        if (!m->planned) mat_plan(c, m);
+        const long long n = m->rows, cols = m->cols;
+        long long b = 8 * cols + 8 * n;  // x gathered once, y written once
+        switch (m->kind) {
+            case SPMV_STENCIL:  // 5 band planes + mask byte per row, CSR tail (row ptr + entries)
+                b += 41 * n + 4 * (n + 1) + 12 * (long long)m->st_eci.n;
+                break;
+            case SPMV_SELL:  // padded 32-row slices + slice offsets + row lengths
+                b += 12 * (long long)m->sell_ci.n + 4 * (long long)m->sell_off.n + 4 * (n + 1);
+                break;
+            case SPMV_SELLW:  // SELL-sigma slices + slot->row permutation + long rows in CSR
+                b += 12 * (long long)m->sell_ci.n + 4 * (long long)m->sell_off.n + 4 * (long long)m->perm.n +
+                     4 * (n + 1);
+                break;
+            default:  // CSR-adaptive: the CSR itself + chunk metadata
+                b += 12 * (long long)m->nnz + 4 * (n + 1) + 16 * (long long)m->n_blocks;
+                break;
+        }
+        *bytes = b;
+        if (kind) *kind = m->kind;
+    });
+}
+
 int ibmgpu_csr_download(ibmgpu_ctx_t c, ibmgpu_mat_t m, int* rp, int* ci, double* v) {
     return guard(c, [&] {
         need(m != nullptr, "csr_download: null matrix");

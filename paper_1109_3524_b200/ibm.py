@@ -211,6 +211,12 @@ class SparseMatrix:
         self.ctx.check(fn(self.ctx.h, *args, C.byref(h)))
         return SparseMatrix(h, self.ctx)
 
+    def format_bytes(self) -> tuple[int, int]:
+        """(bytes one SpMV moves in the device format, SpMV kind) — ibmgpu_csr_format_bytes"""
+        b, k = C.c_longlong(), C.c_int()
+        self.ctx.check(self.ctx.lib.ibmgpu_csr_format_bytes(self.ctx.h, self.h, C.byref(b), C.byref(k)))
+        return b.value, k.value
+
     def transpose(self) -> "SparseMatrix":
         return self._new(self.ctx.lib.ibmgpu_transpose, self.h)
 
