@@ -498,7 +498,7 @@ def main():
                 sys.path.insert(0, os.path.join(ROOT, "tools"))
                 import sweep as _sweep
                 keys = ("grid", "setup_s", "cg_iters_per_s", "cg_iteration_ms", "cg_frac_measured", "spmv_lhs2_us",
-                        "spmv_format_gbs", "spmv_format_frac_measured", "steps_per_s")
+                        "spmv_format_gbs", "spmv_format_frac_measured", "spmv_format_frac_of_8tbs", "steps_per_s")
                 out["grid_sweep"] = [{k: r[k] for k in keys}
                                      for r in _sweep.sweep([1024, 2048, 4096, 8192], spmv_reps=10)]
             except Exception as e:

@@ -75,7 +75,9 @@ def sweep(sizes, spmv_reps=20, emit=None):
             "spmv_lhs2_us": round(spmv_ms * 1e3, 1),
             # roofline of the SpMV on the bytes its format moves (no column indices in the band)
             "spmv_format_gbs": round(fb / (spmv_ms * 1e-3) / 1e9, 1),
+            # (a read-dominated stream can exceed the copy-measured peak, which pays for writes)
             "spmv_format_frac_measured": round(fb / (spmv_ms * 1e-3) / 1e9 / peak, 4),
+            "spmv_format_frac_of_8tbs": round(fb / (spmv_ms * 1e-3) / 8e12, 4),
             # reference-CSR bytes (12/nnz) per second: a CSR-equivalent rate, not a roofline fraction
             "spmv_csr_equiv_gbs": round(sb / (spmv_ms * 1e-3) / 1e9, 1),
             "steps_per_s": round(1e3 / step_ms, 3), "solve2_iters_per_step": [rr.solve2_iters for rr in reps],
