@@ -100,7 +100,8 @@ int ibmgpu_csr_download(ibmgpu_ctx_t ctx, ibmgpu_mat_t m, int* rptr, int* cidx, 
 int ibmgpu_csr_destroy(ibmgpu_ctx_t ctx, ibmgpu_mat_t m);
 /* bytes one SpMV moves in the matrix's device format (plan arrays as stored, x read once, y
  * written once) — the format-actual counterpart of the reference-CSR algorithmic bytes;
- * kind: 0 SELL-32, 2 SELL-32-sigma, 3 stencil/DIA hybrid, else CSR-adaptive */
+ * kind: 0 SELL-32, 2 SELL-32-sigma, 3 stencil/DIA hybrid, else CSR-adaptive; +16 when the slices
+ * carry 16-bit column codes */
 int ibmgpu_csr_format_bytes(ibmgpu_ctx_t ctx, ibmgpu_mat_t m, long long* bytes, int* kind);
 /* SparseMatrix::spmv_into (sparse.hpp:101-110): y = A x, device pointers */
 int ibmgpu_spmv(ibmgpu_ctx_t ctx, ibmgpu_mat_t A, const double* x_dev, double* y_dev);

@@ -199,19 +199,20 @@ int ibmgpu_csr_format_bytes(ibmgpu_ctx_t c, ibmgpu_mat_t m, long long* bytes, in
             case SPMV_STENCIL:  // 5 band planes + mask byte per row, CSR tail (row ptr + entries)
                 b += 41 * n + 4 * (n + 1) + 12 * (long long)m->st_eci.n;
                 break;
-            case SPMV_SELL:  // padded 32-row slices + slice offsets + row lengths
-                b += 12 * (long long)m->sell_ci.n + 4 * (long long)m->sell_off.n + 4 * (n + 1);
+            case SPMV_SELL:  // padded 32-row slices (16- or 32-bit columns) + slice offsets + row lengths
+                b += (m->c16 ? 10 : 12) * (long long)m->sell_v.n + 4 * (long long)m->sell_off.n + 4 * (n + 1) +
+                     4 * (long long)m->sell_cbase.n;
                 break;
             case SPMV_SELLW:  // SELL-sigma slices + slot->row permutation + long rows in CSR
-                b += 12 * (long long)m->sell_ci.n + 4 * (long long)m->sell_off.n + 4 * (long long)m->perm.n +
-                     4 * (n + 1);
+                b += (m->c16 ? 10 : 12) * (long long)m->sell_v.n + 4 * (long long)m->sell_off.n +
+                     4 * (long long)m->perm.n + 4 * (n + 1) + 4 * (long long)m->sell_cbase.n;
                 break;
             default:  // CSR-adaptive: the CSR itself + chunk metadata
                 b += 12 * (long long)m->nnz + 4 * (n + 1) + 16 * (long long)m->n_blocks;
                 break;
         }
         *bytes = b;
-        if (kind) *kind = m->kind;
+        if (kind) *kind = m->kind | (m->c16 ? 16 : 0);
     });
 }
 

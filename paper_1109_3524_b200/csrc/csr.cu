@@ -11,6 +11,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 
@@ -91,6 +92,66 @@ __global__ void k_sell_fill(int rows, const int* __restrict__ rp, const int* __r
             sv[dst] = 0.0;
         }
     }
+}
+
+// ---- 16-bit column codes for SELL / SELL-sigma slices (Mat::c16): one warp per slice; the
+// slice base is the smallest column below tail0 among its real entries; every entry must land
+// in [base, base + 0x8000) or in the top region [tail0, tail0 + 0x8000), else *fail is set.
+__global__ void k_c16_build(int n_slices, int n_slots, const int* __restrict__ rp, const int* __restrict__ perm,
+                            const int* __restrict__ off, const int* __restrict__ sci, int tail0,
+                            unsigned short* __restrict__ code, int* __restrict__ cbase, int* __restrict__ fail) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= n_slices) return;
+    const int slot = w * 32 + lane;
+    const int row = slot < n_slots ? (perm ? perm[slot] : slot) : -1;
+    const int len = row >= 0 ? rp[row + 1] - rp[row] : 0;
+    const int o = off[w], width = (off[w + 1] - o) >> 5;
+    int mn = INT_MAX;
+    for (int k = 0; k < len; ++k) {
+        const int col = sci[o + 32 * k + lane];
+        if (col < tail0) mn = min(mn, col);
+    }
+    for (int d = 16; d > 0; d >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, d));
+    const int base = mn == INT_MAX ? 0 : mn;
+    if (lane == 0) cbase[w] = base;
+    for (int k = 0; k < width; ++k) {
+        unsigned short cd = 0;
+        if (k < len) {
+            const int col = sci[o + 32 * k + lane];
+            if (col - base >= 0 && col - base < 0x8000)
+                cd = (unsigned short)(col - base);
+            else if (col >= tail0 && col - tail0 < 0x8000)
+                cd = (unsigned short)(0x8000 + (col - tail0));
+            else
+                *fail = 1;
+        }
+        code[o + 32 * k + lane] = cd;
+    }
+}
+
+// Replace the slices' int32 columns by 16-bit codes when every entry fits (see Mat::c16).
+void try_c16(Ctx* c, Mat* m, int n_slots) {
+    static const bool off_env = [] {
+        const char* e = std::getenv("IBMGPU_C16");  // IBMGPU_C16=0: keep 32-bit columns (A/B)
+        return e && e[0] == '0';
+    }();
+    if (off_env || m->sell_ci.n == 0) return;
+    const int n_slices = (n_slots + 31) / 32;
+    const int tail0 = m->cols > 0x8000 ? m->cols - 0x8000 : 0;
+    DBuf<unsigned short> code(c, m->sell_ci.n);
+    DBuf<int> base(c, (size_t)std::max(n_slices, 1)), fail(c, 1);
+    CK(cudaMemsetAsync(fail.p, 0, sizeof(int), c->stream));
+    k_c16_build<<<(n_slices * 32 + 255) / 256, 256, 0, c->stream>>>(n_slices, n_slots, m->rp.p,
+                                                                    m->kind == SPMV_SELLW ? m->perm.p : nullptr,
+                                                                    m->sell_off.p, m->sell_ci.p, tail0, code.p,
+                                                                    base.p, fail.p);
+    CK_LAUNCH(c);
+    if (d2h_scalar(c, fail.p)) return;
+    m->sell_c16 = std::move(code);
+    m->sell_cbase = std::move(base);
+    m->c16_tail0 = tail0;
+    m->c16 = true;
+    m->sell_ci.release();
 }
 
 // ---- stencil (DIA-hybrid) plan: classify each row against the band {i-S,i-1,i,i+1,i+S}
@@ -274,6 +335,7 @@ void mat_plan(Ctx* c, Mat* m) {
                                                                         m->sell_off.p, nullptr, m->sell_ci.p,
                                                                         m->sell_v.p);
         CK_LAUNCH(c);
+        try_c16(c, m, m->rows);
         return;
     }
     std::vector<int> rp(static_cast<size_t>(m->rows) + 1);
@@ -339,6 +401,7 @@ void mat_plan(Ctx* c, Mat* m) {
                 k_sell_fill<<<(ss * 32 + 255) / 256, 256, 0, c->stream>>>(ns, m->rp.p, m->ci.p, m->v.p, m->sell_off.p,
                                                                           m->perm.p, m->sell_ci.p, m->sell_v.p);
                 CK_LAUNCH(c);
+                try_c16(c, m, ns);
                 sync(c);
                 return;
             }

@@ -144,6 +144,13 @@ struct ibmgpu_mat {
     ibmgpu::DBuf<int> sell_off;  // n_slices + 1 element offsets
     ibmgpu::DBuf<int> sell_ci;
     ibmgpu::DBuf<double> sell_v;
+    // 16-bit column codes (csr.cu try_c16): code < 0x8000 -> slice base + code, else
+    // c16_tail0 + code - 0x8000 (the last 32768 columns: the body tail of the SA levels). When a
+    // matrix's columns fit, sell_ci is dropped and the SELL kernels stream 10 B per entry, not 12.
+    bool c16 = false;
+    int c16_tail0 = 0;
+    ibmgpu::DBuf<unsigned short> sell_c16;
+    ibmgpu::DBuf<int> sell_cbase;  // per slice
     ibmgpu::DBuf<int> perm;              // SELL-sigma: slot -> original row
     int n_short = 0;                     // SELL-sigma slots (rows <= 96 entries)
     int n_long = 0;                      // rows > 96 entries: one warp each, in-order sum
@@ -175,6 +182,7 @@ inline void mat_rehome(Mat* m, cudaStream_t s) {
         if (b.p) b.s = s;
     };
     set(m->rp), set(m->ci), set(m->v), set(m->sell_off), set(m->sell_ci), set(m->sell_v), set(m->perm);
+    set(m->sell_c16), set(m->sell_cbase);
     set(m->long_rows), set(m->st_v), set(m->st_mask), set(m->st_erp), set(m->st_eci), set(m->st_ev);
     set(m->blk_meta), set(m->lrow), set(m->lpart), set(m->lcnt);
 }

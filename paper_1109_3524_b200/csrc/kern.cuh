@@ -223,15 +223,34 @@ struct XJacobi {
 // Epi::NR > 0 enables a fused grid reduction: epi.row adds into acc[0..NR), and epi.fin(tot)
 // runs once in the last block.
 
+// Column sources of the SELL kernels: plain int32 indices, or 16-bit codes against a per-slice
+// base (Mat::c16). ld() loads the raw entry, dec() turns it into the column.
+struct Cols32 {
+    const int* ci;
+    const int* cbase;  // unused
+    int tail0;
+    __device__ __forceinline__ int ld(int k) const { return __ldg(ci + k); }
+    __device__ __forceinline__ int base(int) const { return 0; }
+    __device__ __forceinline__ int dec(int raw, int) const { return raw; }
+};
+struct Cols16 {
+    const unsigned short* c;
+    const int* cbase;
+    int tail0;
+    __device__ __forceinline__ int ld(int k) const { return (int)__ldg(c + k); }
+    __device__ __forceinline__ int base(int slice) const { return __ldg(cbase + slice); }
+    __device__ __forceinline__ int dec(int raw, int b) const { return raw < 0x8000 ? b + raw : tail0 + (raw - 0x8000); }
+};
+
 // SELL-32, thread per row, kSellRows rows per thread: every load of both rows (slice entries,
 // epilogue operands) is issued before the first use, doubling the bytes in flight per thread —
 // the level-0 kernels are latency-bound otherwise (ncu: 33% DRAM, long-scoreboard stalls).
 constexpr int kSellRows = 1;
 constexpr int kSellU = 5;  // entries per row loaded up front (5-point rows); wider rows loop
 
-template <class XF, class Epi>
+template <class XF, class Epi, class CS = Cols32>
 __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __restrict__ rp,
-                                                         const int* __restrict__ off, const int* __restrict__ ci,
+                                                         const int* __restrict__ off, CS cs,
                                                          const double* __restrict__ v, XF xf, Epi epi) {
     pdl_release_early(8);
     constexpr int NR = Epi::NR;
@@ -241,7 +260,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
     // The matrix is constant for the whole solve, so its first slice entries are loaded BEFORE
     // griddepcontrol.wait: under PDL they stream in while the predecessor kernel drains.
     const int n_slices = (rows + 31) >> 5;
-    int ix[kSellRows], base[kSellRows], width[kSellRows], len[kSellRows];
+    int ix[kSellRows], base[kSellRows], width[kSellRows], len[kSellRows], cb[kSellRows];
 #pragma unroll
     for (int q = 0; q < kSellRows; ++q) {
         const int i = (blockIdx.x * kSellRows + q) * kBlock + threadIdx.x;
@@ -250,6 +269,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
         // masks the accumulation, so neither waits on row_ptr
         const int beg = sl < n_slices ? __ldg(off + sl) : 0;
         width[q] = sl < n_slices ? (__ldg(off + sl + 1) - beg) >> 5 : 0;
+        cb[q] = sl < n_slices ? cs.base(sl) : 0;
         base[q] = beg + (i & 31);
         len[q] = i < rows ? __ldg(rp + i + 1) - __ldg(rp + i) : 0;
         ix[q] = i;
@@ -261,7 +281,7 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
 #pragma unroll
         for (int u = 0; u < kSellU; ++u)
             if (u < width[q]) {
-                c[q][u] = __ldg(ci + base[q] + 32 * u);
+                c[q][u] = cs.ld(base[q] + 32 * u);
                 a[q][u] = __ldg(v + base[q] + 32 * u);
             }
     pdl_wait();
@@ -278,9 +298,9 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_sell(int rows, const int* __
         s[q] = 0.0;
 #pragma unroll
         for (int u = 0; u < kSellU; ++u)
-            if (u < len[q]) s[q] = addd(s[q], mul(a[q][u], xf(c[q][u])));
+            if (u < len[q]) s[q] = addd(s[q], mul(a[q][u], xf(cs.dec(c[q][u], cb[q]))));
         for (int k = kSellU; k < len[q]; ++k)  // rows wider than kSellU (body-coupled rows)
-            s[q] = addd(s[q], mul(__ldg(v + base[q] + 32 * k), xf(__ldg(ci + base[q] + 32 * k))));
+            s[q] = addd(s[q], mul(__ldg(v + base[q] + 32 * k), xf(cs.dec(cs.ld(base[q] + 32 * k), cb[q]))));
     }
     if (skip) return;
 #pragma unroll
@@ -403,10 +423,10 @@ __device__ __forceinline__ double row_sum_inorder(int row, const int* __restrict
 #ifndef IBMGPU_SELLW_MINB
 #define IBMGPU_SELLW_MINB 4
 #endif
-template <class XF, class Epi, int kU = 4>
+template <class XF, class Epi, int kU = 4, class CS = Cols32>
 __global__ void __launch_bounds__(kBlock, kU == 4 ? IBMGPU_SELLW_MINB : 2) k_spmv_sellw(int rows, const int* __restrict__ rp,
                                                           const int* __restrict__ perm, const int* __restrict__ off,
-                                                          const int* __restrict__ ci, const double* __restrict__ v,
+                                                          CS cs, const double* __restrict__ v,
                                                           XF xf, Epi epi, int sblocks, const int* __restrict__ long_rows,
                                                           int n_long, const int* __restrict__ csr_ci,
                                                           const double* __restrict__ csr_v) {
@@ -438,6 +458,7 @@ __global__ void __launch_bounds__(kBlock, kU == 4 ? IBMGPU_SELLW_MINB : 2) k_spm
     const int beg = in_slice ? __ldg(off + sl) : 0;
     const int width = in_slice ? (__ldg(off + sl + 1) - beg) >> 5 : 0;
     const int base = beg + (i & 31);
+    const int cb = in_slice ? cs.base(sl) : 0;
     const int row = i < rows ? __ldg(perm + i) : -1;
     const int len = row >= 0 ? __ldg(rp + row + 1) - __ldg(rp + row) : 0;
     int c0[U];
@@ -445,7 +466,7 @@ __global__ void __launch_bounds__(kBlock, kU == 4 ? IBMGPU_SELLW_MINB : 2) k_spm
 #pragma unroll
     for (int u = 0; u < U; ++u)
         if (u < width) {
-            c0[u] = __ldg(ci + base + 32 * u);
+            c0[u] = cs.ld(base + 32 * u);
             a0[u] = __ldg(v + base + 32 * u);
         }
     pdl_wait();  // everything above is the (constant) matrix
@@ -460,12 +481,12 @@ __global__ void __launch_bounds__(kBlock, kU == 4 ? IBMGPU_SELLW_MINB : 2) k_spm
 #pragma unroll
         for (int u = 0; u < U; ++u)
             if (k0 + U + u < width) {
-                c1[u] = __ldg(ci + base + 32 * (k0 + U + u));
+                c1[u] = cs.ld(base + 32 * (k0 + U + u));
                 a1[u] = __ldg(v + base + 32 * (k0 + U + u));
             }
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            if (k0 + u < len) s = addd(s, mul(a0[u], xf(c0[u])));
+            if (k0 + u < len) s = addd(s, mul(a0[u], xf(cs.dec(c0[u], cb))));
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             c0[u] = c1[u];
@@ -619,10 +640,16 @@ template <class XF, class Epi>
 inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
     if (A->rows == 0) return;
     int grid = 0;
+    const Cols32 c32{A->sell_ci.p, nullptr, 0};
+    const Cols16 c16{A->sell_c16.p, A->sell_cbase.p, A->c16_tail0};
     if (A->kind == SPMV_SELL) {
         grid = (A->rows + kSellRows * kBlock - 1) / (kSellRows * kBlock);
-        launch_k(c, k_spmv_sell<XF, Epi>, grid, kBlock, s, A->rows, A->rp.p, A->sell_off.p, A->sell_ci.p, A->sell_v.p,
-                 xf, epi);
+        if (A->c16)
+            launch_k(c, k_spmv_sell<XF, Epi, Cols16>, grid, kBlock, s, A->rows, A->rp.p, A->sell_off.p, c16,
+                     A->sell_v.p, xf, epi);
+        else
+            launch_k(c, k_spmv_sell<XF, Epi, Cols32>, grid, kBlock, s, A->rows, A->rp.p, A->sell_off.p, c32,
+                     A->sell_v.p, xf, epi);
     } else if (A->kind == SPMV_STENCIL) {
         const StencilPlan P{A->st_v.p, A->st_mask.p, A->st_erp.p, A->st_eci.p, A->st_ev.p, A->st_S1, A->st_S2};
         grid = (A->rows + kBlock - 1) / kBlock;
@@ -630,14 +657,22 @@ inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
     } else if (A->kind == SPMV_SELLW) {
         const int sb = (A->n_short + kBlock - 1) / kBlock;
         grid = sb + (A->n_long + kBlock / 32 - 1) / (kBlock / 32);
-        if (A->n_short < c->num_sms * 1024 && A->nnz >= 40ll * A->rows)  // few, long rows
-            launch_k(c, k_spmv_sellw<XF, Epi, 8>, grid, kBlock, s, A->n_short, A->rp.p, A->perm.p, A->sell_off.p,
-                     A->sell_ci.p, A->sell_v.p, xf, epi, sb, (const int*)A->long_rows.p, A->n_long,
-                     (const int*)A->ci.p, (const double*)A->v.p);
-        else
-            launch_k(c, k_spmv_sellw<XF, Epi, 4>, grid, kBlock, s, A->n_short, A->rp.p, A->perm.p, A->sell_off.p,
-                     A->sell_ci.p, A->sell_v.p, xf, epi, sb, (const int*)A->long_rows.p, A->n_long,
-                     (const int*)A->ci.p, (const double*)A->v.p);
+        const bool wide = A->n_short < c->num_sms * 1024 && A->nnz >= 40ll * A->rows;  // few, long rows
+        auto go = [&](auto kern, auto cs) {
+            launch_k(c, kern, grid, kBlock, s, A->n_short, A->rp.p, A->perm.p, A->sell_off.p, cs, A->sell_v.p, xf,
+                     epi, sb, (const int*)A->long_rows.p, A->n_long, (const int*)A->ci.p, (const double*)A->v.p);
+        };
+        if (A->c16) {
+            if (wide)
+                go(k_spmv_sellw<XF, Epi, 8, Cols16>, c16);
+            else
+                go(k_spmv_sellw<XF, Epi, 4, Cols16>, c16);
+        } else {
+            if (wide)
+                go(k_spmv_sellw<XF, Epi, 8, Cols32>, c32);
+            else
+                go(k_spmv_sellw<XF, Epi, 4, Cols32>, c32);
+        }
     } else {
         const AdaptPlan pl{A->blk_meta.p, A->lrow.p, A->lpart.p, A->lcnt.p};
         grid = A->n_blocks;
