@@ -21,6 +21,7 @@ all: $(PKG)/libibmgpu.so oracle
 
 # the stepper's explicit-term kernels must round like the reference (no FMA contraction)
 $(OBJDIR)/stepper.o: NVEXTRA := --fmad=false
+$(OBJDIR)/assemble.o: NVEXTRA := --fmad=false
 
 $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p $(OBJDIR)

@@ -15,6 +15,7 @@
 #include <string>
 
 #include "internal.cuh"
+#include "refresh.cuh"
 #include "kern.cuh"
 
 namespace ibmgpu {
@@ -219,7 +220,11 @@ void coupled_system(Ctx* c, const Mat* G, const Mat* E, const Mat* BN, int pin_i
     delete Et;
     *QT = transpose(c, *Q);
     const int slice = slice_rows > 0 ? slice_rows : (*QT)->rows;
-    Mat* raw = triple_product(c, *QT, BN, *Q, std::max(slice, 1), peak, nullptr);
+    // Full-height product without slice statistics: every row of QT B^N Q has a few dozen products,
+    // so the warp-per-row Gustavson kernel (refresh.cu; same order, same rounding) does it in one
+    // pass instead of expand-sort-compress chunks (C5-8192: 2.4 s -> see DESIGN §(f)4).
+    Mat* raw = (slice >= (*QT)->rows && !peak) ? triple_small(c, *QT, BN, *Q)
+                                               : triple_product(c, *QT, BN, *Q, std::max(slice, 1), peak, nullptr);
     Mat* sym = symmetrized(c, raw);
     delete raw;
     *lhs2 = pin(c, sym, pin_idx);

@@ -962,7 +962,65 @@ Mat* add(Ctx* c, double a, const Mat* A, double b, const Mat* B) {
     return finish_plan(c, m);
 }
 
+namespace {
+// symmetrized() for a structurally symmetric A without forming A^T: entry (i, j) pairs with (j, i),
+// found by binary search in row j; the sum is (0 + 0.5 a_ij) + 0.5 a_ji with exact zeros dropped,
+// exactly what add_sparse(0.5, A, 0.5, A^T) computes (sparse.hpp:317-329, 351-353). An entry
+// without a partner sets *asym and the caller takes the transpose path.
+__global__ void k_sym_pairs(int rows, const int* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ v, int* __restrict__ cnt, const int* __restrict__ orp,
+                            int* __restrict__ oci, double* __restrict__ ov, int* __restrict__ asym) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    int n = 0;
+    const int o = orp ? orp[i] : 0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int j = ci[k];
+        int lo = rp[j], hi = rp[j + 1];
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (ci[mid] < i)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        if (lo == rp[j + 1] || ci[lo] != i) {
+            *asym = 1;
+            return;
+        }
+        const double s = addd(addd(0.0, mul(0.5, v[k])), mul(0.5, v[lo]));
+        if (s != 0.0) {
+            if (oci) {
+                oci[o + n] = j;
+                ov[o + n] = s;
+            }
+            ++n;
+        }
+    }
+    if (cnt) cnt[i] = n;
+}
+}  // namespace
+
 Mat* symmetrized(Ctx* c, const Mat* A) {
+    if (A->rows == A->cols && A->rows > 0) {
+        const int rows = A->rows;
+        DBuf<int> cnt(c, (size_t)rows + 1), asym(c, 1);
+        CK(cudaMemsetAsync(asym.p, 0, sizeof(int), c->stream));
+        k_sym_pairs<<<blocks(rows), 256, 0, c->stream>>>(rows, A->rp.p, A->ci.p, A->v.p, cnt.p, nullptr, nullptr,
+                                                         nullptr, asym.p);
+        CK_LAUNCH(c);
+        if (!d2h_scalar(c, asym.p)) {
+            Mat* m = mat_new(c, rows, rows, 0);
+            exclusive_scan_total(c, cnt.p, m->rp.p, rows);
+            m->nnz = d2h_scalar(c, m->rp.p + rows);
+            m->ci.alloc(c, (size_t)std::max(m->nnz, 1));
+            m->v.alloc(c, (size_t)std::max(m->nnz, 1));
+            k_sym_pairs<<<blocks(rows), 256, 0, c->stream>>>(rows, A->rp.p, A->ci.p, A->v.p, nullptr, m->rp.p,
+                                                             m->ci.p, m->v.p, asym.p);
+            CK_LAUNCH(c);
+            return finish_plan(c, m);
+        }
+    }
     Mat* At = transpose(c, A);
     Mat* S = add(c, 0.5, A, 0.5, At);
     delete At;

@@ -31,6 +31,7 @@
 #include "kern.cuh"
 #include "pcg.cuh"
 #include "refresh.cuh"
+#include "assemble.cuh"
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -570,8 +571,12 @@ struct ibmgpu_stepper {
         QT = QTn;
         lhs2 = L2n;
         lap("free");
-        for (Mat* m : {Q, QT, lhs2}) mat_plan(c, m);
-        lap("plans");
+        mat_plan(c, Q);
+        lap("plan Q");
+        mat_plan(c, QT);
+        lap("plan QT");
+        mat_plan(c, lhs2);
+        lap("plan lhs2");
     }
 
     Mat* ensure_H() {
@@ -693,15 +698,6 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
     S->n_lambda = S->n_p + 2 * S->n_b;
     for (const auto& b : S->bodies) S->geom_static_after = std::max(S->geom_static_after, b.static_after());
 
-    // host grid operators
-    std::vector<ibmhost::BcCoupling> vbc;
-    const std::vector<double> M = ibmhost::metric(g);
-    const ibmhost::Csr Lh = ibmhost::diffusion(g, vbc);
-    const ibmhost::Csr Gh = ibmhost::gradient(g);
-    lap("host M, L, G");
-    S->L = mat_upload(c, Lh.rows, Lh.cols, (int)Lh.ci.size(), Lh.rp.data(), Lh.ci.data(), Lh.v.data());
-    S->G = mat_upload(c, Gh.rows, Gh.cols, (int)Gh.ci.size(), Gh.rp.data(), Gh.ci.data(), Gh.v.data());
-
     // grid arrays on the device
     auto up = [&](DBuf<double>& d, const std::vector<double>& h) {
         d.alloc(c, h.size());
@@ -711,7 +707,13 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
     up(S->dy, g.dy);
     up(S->del_x, g.del_x);
     up(S->del_y, g.del_y);
-    lap("upload L, G, grid");
+    // M, L (with its wall couplings) and G assembled on the device (assemble.cu, operators.hpp:75-228)
+    S->bl.init(g.nx, g.ny);
+    const int slot_off[8] = {S->bl.lu, S->bl.ru, S->bl.lv, S->bl.rv, S->bl.bv, S->bl.tv, S->bl.bu, S->bl.tu};
+    GridOps gops = assemble_grid_ops(c, g.nx, g.ny, S->dx.p, S->dy.p, S->del_x.p, S->del_y.p, slot_off);
+    S->L = gops.L;
+    S->G = gops.G;
+    lap("device M, L, G");
 
     // A = M/dt - (nu/2) L ; B^N (operators.hpp:350-374) on the device; M/dt, 1/M and dt/M are
     // formed from M on the device with the reference's rounding (one IEEE op each)
@@ -720,8 +722,7 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
     require(S->n_order >= 1 && S->n_order <= 3, "operators: B^N order must be 1, 2 or 3");
     DBuf<double> dd(c, nq), mi(c, nq);
     {
-        DBuf<double> Md(c, nq);
-        h2d(c, Md.p, M.data(), nq);
+        const DBuf<double>& Md = gops.M;
         S->mdt.alloc(c, nq);
         k_metric_terms<<<blocks((long long)nq), 256, 0, c->stream>>>((long long)nq, Md.p, S->dt, S->mdt.p, mi.p, dd.p);
         CK_LAUNCH(c);
@@ -789,7 +790,6 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
     lap("SA hierarchy");
 
     // boundary + state
-    S->bl.init(g.nx, g.ny);
     const ibmhost::Boundary b0 = ibmhost::Boundary::initial(g, cfg.bc);
     up(S->bnd, b0.packed());
     S->bnd_n.alloc(c, (size_t)S->bl.total);
@@ -809,34 +809,12 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
     if (S->ek.kind[3]) S->max_cfl = std::max(S->max_cfl, cfg.bc.u_inf * S->dt / g.dy[g.ny - 1]);
     if (S->ek.kind[2]) S->max_cfl = std::max(S->max_cfl, cfg.bc.u_inf * S->dt / g.dy[0]);
 
-    // viscous boundary couplings grouped by row in list order
-    {
-        std::vector<int> order(vbc.size());
-        std::iota(order.begin(), order.end(), 0);
-        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return vbc[a].row < vbc[b].row; });
-        std::vector<int> rows, off{0}, pos;
-        std::vector<double> coeff;
-        const int slot_off[8] = {S->bl.lu, S->bl.ru, S->bl.lv, S->bl.rv, S->bl.bv, S->bl.tv, S->bl.bu, S->bl.tu};
-        for (size_t k = 0; k < order.size(); ++k) {
-            const auto& e = vbc[order[k]];
-            if (rows.empty() || rows.back() != e.row) {
-                if (!rows.empty()) off.push_back((int)pos.size());
-                rows.push_back(e.row);
-            }
-            pos.push_back(slot_off[e.slot] + e.idx);
-            coeff.push_back(e.coeff);
-        }
-        off.push_back((int)pos.size());
-        S->vb_n = (int)rows.size();
-        S->vb_rows.alloc(c, rows.size() + 1);
-        S->vb_off.alloc(c, off.size());
-        S->vb_pos.alloc(c, pos.size() + 1);
-        S->vb_coeff.alloc(c, coeff.size() + 1);
-        h2d(c, S->vb_rows.p, rows.data(), rows.size());
-        h2d(c, S->vb_off.p, off.data(), off.size());
-        h2d(c, S->vb_pos.p, pos.data(), pos.size());
-        h2d(c, S->vb_coeff.p, coeff.data(), coeff.size());
-    }
+    // viscous boundary couplings grouped by row in list order (assembled with L on the device)
+    S->vb_n = gops.n_wall_rows;
+    S->vb_rows = std::move(gops.wall_rows);
+    S->vb_off = std::move(gops.wall_off);
+    S->vb_pos = std::move(gops.wall_pos);
+    S->vb_coeff = std::move(gops.wall_coeff);
     S->bcn.alloc(c, nq);
     S->bcnp1.alloc(c, nq);
     CK(cudaMemsetAsync(S->bcn.p, 0, sizeof(double) * nq, c->stream));
