@@ -112,7 +112,7 @@ struct EpiJacobiResidual {  // K1: x_i = wd_i b_i ; r_i = b_i - s
     double* x;
     double* r;
     const int* done;
-    __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ bool skip() const { return done && flag_set(done); }
     __device__ void touch(int i) const {
         pf(wd + i);
         pf(b + i);
@@ -130,7 +130,7 @@ struct EpiStoreSkip {  // K2: b_{l+1} = s
     static constexpr int NR = 0;
     double* y;
     const int* done;
-    __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ bool skip() const { return done && flag_set(done); }
     __device__ void row(int i, double s, double*) const { y[i] = s; }
     __device__ RedSlot slot() const { return {}; }
     __device__ void fin(double*) const {}
@@ -142,7 +142,7 @@ struct EpiStoreJacobi {  // K2 into level l+1: b_i = s and the pre-smoothed iter
     const double* wd;
     double* xj;
     const int* done;
-    __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ bool skip() const { return done && flag_set(done); }
     __device__ void touch(int i) const { pf(wd + i); }
     __device__ void row(int i, double s, double*) const {
         y[i] = s;
@@ -156,7 +156,7 @@ struct EpiAddInPlace {  // K3: x_i += s
     static constexpr int NR = 0;
     double* x;
     const int* done;
-    __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ bool skip() const { return done && flag_set(done); }
     __device__ void touch(int i) const { pf(x + i); }
     __device__ void row(int i, double s, double*) const { x[i] = addd(x[i], s); }
     __device__ RedSlot slot() const { return {}; }
@@ -170,7 +170,7 @@ struct EpiPostSmooth {  // K4: out_i = x_i + wd_i (b_i - s)
     const double* x;
     double* out;
     const int* done;
-    __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ bool skip() const { return done && flag_set(done); }
     __device__ void touch(int i) const {
         pf(wd + i);
         pf(b + i);
@@ -191,7 +191,7 @@ struct EpiPostSmoothDot {
     const int* done;
     RedSlot rs;
     Fin f;
-    __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ bool skip() const { return done && flag_set(done); }
     __device__ void touch(int i) const {
         pf(wd + i);
         pf(b + i);

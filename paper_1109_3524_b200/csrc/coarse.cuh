@@ -119,7 +119,7 @@ __device__ __forceinline__ void coarse_chunk(const Phase& P, int blk) {
 }
 
 static __global__ void __launch_bounds__(kBlock) k_coarse_cycle(CoarsePlan cp, const int* done) {
-    if (done && *(volatile const int*)done) return;  // uniform: set before this launch
+    if (done && flag_set(done)) return;  // uniform: set before this launch
     for (int ph = 0; ph < cp.n_phases; ++ph) {
         const Phase& P = cp.phases[ph];
         if (P.kind == PH_GEMV) {

@@ -196,7 +196,7 @@ __global__ void k_symmetrize_lower(int n, double* A) {
 // warp per row GEMV y = A x (A row-major n x n); x staged through shared memory in chunks.
 __global__ void __launch_bounds__(256) k_gemv(int n, const double* __restrict__ A, const double* __restrict__ x,
                                               double* __restrict__ y, const int* done) {
-    if (done && *(volatile const int*)done) return;
+    if (done && flag_set(done)) return;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= n) return;
     const double* row = A + (size_t)warp * n;
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(128) k_symv_tiles(int n, int nt, const double*
                      : "memory");
     }
     pdl_wait();
-    const bool skip = done && *(volatile const int*)done;  // x is read regardless: one round trip
+    const bool skip = done && flag_set(done);  // x is read regardless: one round trip
     if (threadIdx.x < TS) {
         const int gi = I * TS + threadIdx.x, gj = J * TS + threadIdx.x;
         xi[threadIdx.x] = gi < n ? x[gi] : 0.0;
@@ -299,7 +299,7 @@ __global__ void k_symv_combine(int n, int nt, const double* __restrict__ prow, c
                                double* __restrict__ y, const int* done) {
     pdl_release_early(8);
     pdl_wait();
-    const bool skip = done && *(volatile const int*)done;  // tested after the partial loads
+    const bool skip = done && flag_set(done);  // tested after the partial loads
     const int I = blockIdx.x, r = threadIdx.x;
     if (r >= TS) return;
     double s = 0.0;

@@ -150,7 +150,7 @@ struct FinStore {
     }
 };
 
-__device__ __forceinline__ bool is_done(const PcgState* S) { return *(volatile const int*)&S->done != 0; }
+__device__ __forceinline__ bool is_done(const PcgState* S) { return flag_set(&S->done); }
 
 struct EpiDInit {  // r = b - A x ; partial b.b, r.r
     static constexpr int NR = 2;

@@ -38,6 +38,12 @@ constexpr unsigned kFull = 0xffffffffu;
 // the matrix stream (epilogues opt in by defining touch(i)).
 __device__ __forceinline__ void pf(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 
+// The PCG's done flag, written by the previous kernel of the graph: after griddepcontrol.wait a
+// weak L2 load (ld.global.cg) sees it. A volatile load compiles to a system-scope strong load
+// (LDG.E.STRONG.SYS) whose latency stalled every warp of the coarse-level SpMVs (ncu: 15% of the
+// stall samples of the level-3 adaptive kernel at S-4M).
+__device__ __forceinline__ bool flag_set(const int* p) { return __ldcg(p) != 0; }
+
 // Programmatic dependent launch: every hot-path kernel is launched with programmatic stream
 // serialization, waits for its predecessor's completion + memory flush before touching memory
 // (griddepcontrol.wait), and releases its successor when its own block is done — so the next

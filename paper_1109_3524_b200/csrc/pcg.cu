@@ -85,7 +85,7 @@ struct BodyInitZ {
     double* p;
     RedSlot rs;
     PcgState* st;
-    __device__ bool skip() const { return st->done != 0; }
+    __device__ bool skip() const { return flag_set(&st->done); }
     __device__ void row(int i, double* acc) const {
         const double ri = r[i];
         const double zi = invd ? mul(ri, invd[i]) : ri;
@@ -102,7 +102,7 @@ struct BodyCopy {  // p = z (after the initial V-cycle)
     const double* z;
     double* p;
     const PcgState* st;
-    __device__ bool skip() const { return st->done != 0; }
+    __device__ bool skip() const { return flag_set(&st->done); }
     __device__ void row(int i, double*) const { p[i] = z[i]; }
     __device__ RedSlot slot() const { return {}; }
     __device__ void fin(double*) const {}
@@ -119,7 +119,7 @@ struct EpiSpmvPAp {  // B1
     double* Ap;
     RedSlot rs;
     PcgState* st;
-    __device__ bool skip() const { return st->done != 0; }
+    __device__ bool skip() const { return flag_set(&st->done); }
     __device__ void touch(int i) const { pf(p + i); }
     __device__ void row(int i, double s, double* acc) const {
         Ap[i] = s;
@@ -163,7 +163,7 @@ struct BodyUpdate {  // B2
     int kind;
     RedSlot rs;
     PcgState* st;
-    __device__ bool skip() const { return st->done != 0; }
+    __device__ bool skip() const { return flag_set(&st->done); }
     __device__ void row(int i, double* acc) const {
         const double a = st->alpha;
         x[i] = addd(x[i], mul(a, p[i]));           // axpy(alpha, p, x)
@@ -212,7 +212,7 @@ struct BodyP {  // B4: p = z + beta p
     const double* z;
     double* p;
     const PcgState* st;
-    __device__ bool skip() const { return st->done != 0; }
+    __device__ bool skip() const { return flag_set(&st->done); }
     __device__ void row(int i, double*) const { p[i] = addd(z[i], mul(st->beta, p[i])); }
     __device__ RedSlot slot() const { return {}; }
     __device__ void fin(double*) const {}
@@ -239,7 +239,7 @@ struct BodyDotAfterCoarse {  // no-level hierarchy: r.z after the dense solve
     const int* done;
     RedSlot rs;
     Fin f;
-    __device__ bool skip() const { return done && *(volatile const int*)done; }
+    __device__ bool skip() const { return done && flag_set(done); }
     __device__ void row(int i, double* acc) const { acc[0] += r[i] * z[i]; }
     __device__ RedSlot slot() const { return rs; }
     __device__ void fin(double* tot) const { f(tot); }
