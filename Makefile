@@ -13,8 +13,12 @@ ifeq ($(CHECKED),1)
 CHECKFLAGS := -DIBMGPU_CHECKED=1
 OBJDIR := build/obj_checked
 endif
+# A/B variants: make EXTRA=-D... OBJDIR=build/obj_ab (tools/ab_iter.py with IBMGPU_LIB)
+ifneq ($(EXTRA),)
+OBJDIR := build/obj_ab
+endif
 OBJ := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(SRC)) $(patsubst $(PKG)/csrc/host/%.cpp,$(OBJDIR)/host_%.o,$(HOST))
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC,-fopenmp -Xptxas -v --expt-relaxed-constexpr $(CHECKFLAGS)
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC,-fopenmp -Xptxas -v --expt-relaxed-constexpr $(CHECKFLAGS) $(EXTRA)
 HOSTFLAGS := -O3 -std=c++20 -fPIC -fopenmp -ffp-contract=off
 
 all: $(PKG)/libibmgpu.so oracle

@@ -69,6 +69,22 @@ struct ibmgpu_hier {
 namespace ibmgpu {
 using Hier = ibmgpu_hier;
 
+// A hierarchy built on a helper stream (the stepper's operator pipeline) handed to the main
+// stream: every buffer is then freed in main-stream order (see mat_rehome).
+inline void hier_rehome(Hier* h, cudaStream_t s) {
+    auto set = [s](auto& b) {
+        if (b.p) b.s = s;
+    };
+    for (auto& lv : h->levels) {
+        for (Mat* m : {lv->A, lv->P, lv->Pt})
+            if (m) mat_rehome(m, s);
+        set(lv->invd), set(lv->wd), set(lv->agg), set(lv->b), set(lv->x), set(lv->r), set(lv->xo), set(lv->xj);
+    }
+    if (h->coarse_A) mat_rehome(h->coarse_A, s);
+    set(h->coarse_inv), set(h->coarse_tiles), set(h->prow), set(h->pcol), set(h->cb), set(h->cx), set(h->dense);
+    set(h->phases), set(h->bar);
+}
+
 // Aggregates of the previous build, per level, keyed by the strength graph they came from.
 // aggregate() (amg.hpp:79-107) is a function of the strength graph alone, so when a rebuild's
 // graph is identical to the cached one the cached aggregates ARE the result (moving bodies: the
@@ -80,6 +96,11 @@ struct AggCache {
     };
     std::vector<Lv> lv;
     long long hits = 0, misses = 0;
+    void rehome(cudaStream_t s) {  // buffers freed in the order of the stream that uses them next
+        for (auto& l : lv)
+            for (DBuf<int>* b : {&l.rp, &l.ci, &l.agg})
+                if (b->p) b->s = s;
+    }
 };
 
 // amg_setup.cu

@@ -462,6 +462,7 @@ void plan_adaptive_from(Ctx* c, Mat* m, const std::vector<int>& rp) {
             r = r1;
         }
         m->n_blocks = static_cast<int>(meta.size());
+        m->n_lrows = static_cast<int>(lrow.size());
         m->blk_meta.alloc(c, meta.size());
         h2d(c, m->blk_meta.p, meta.data(), meta.size());
         m->lrow.alloc(c, std::max<size_t>(lrow.size(), 1));

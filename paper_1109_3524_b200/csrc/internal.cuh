@@ -164,6 +164,7 @@ struct ibmgpu_mat {
     ibmgpu::DBuf<int> st_erp, st_eci;    // extras CSR
     ibmgpu::DBuf<double> st_ev;
     int n_blocks = 0;                   // CSR-adaptive plan (kern.cuh k_spmv_adapt)
+    int n_lrows = 0;                    // its split long rows (each owns a reduction slot)
     ibmgpu::DBuf<int4> blk_meta;         // per CTA: {r0, r1, tpr, 0} | {row, chunk, 0, long-row id}
     ibmgpu::DBuf<int2> lrow;             // per long row: {partial base, chunks}
     ibmgpu::DBuf<double> lpart;          // long-row chunk partials

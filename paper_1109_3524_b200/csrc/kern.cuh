@@ -58,10 +58,16 @@ __device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.lau
 constexpr int kNumSms = 148;
 __device__ __forceinline__ bool pdl_early(int bps) { return gridDim.x <= kNumSms * bps; }
 __device__ __forceinline__ void pdl_release_early(int bps) {
+#if !defined(IBMGPU_NO_EARLY_RELEASE)
     if (pdl_early(bps)) pdl_release();
+#endif
 }
 __device__ __forceinline__ void pdl_release_late(int bps) {
+#if !defined(IBMGPU_NO_EARLY_RELEASE)
     if (!pdl_early(bps)) pdl_release();
+#else
+    pdl_release();
+#endif
 }
 
 inline bool pdl_enabled() {
@@ -212,15 +218,28 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(Epi epi, int nblocks) 
 }
 
 // ---------------------------------------------------------------- operand gathers
+// Gathers of vectors produced by the previous kernel: a weak coherent load (ld.global), not the
+// non-coherent __ldg path. Under PDL the producer runs while this grid is already resident, and
+// ld.global.nc assumes the data are read-only for the grid's lifetime — it can return a line
+// cached before the producer wrote it (seen as a diverging amg_solve on a 3758-row system).
+// griddepcontrol.wait makes the producer's writes visible to weak loads.
+__device__ __forceinline__ double ld_weak(const double* p) { return *p; }  // LDG.E.64 (not .CONSTANT)
+#if defined(IBMGPU_X_CG)
+#define IBM_XLD __ldcg
+#elif defined(IBMGPU_X_NC)
+#define IBM_XLD __ldg
+#else
+#define IBM_XLD ld_weak
+#endif
 struct XPlain {
     const double* x;
-    __device__ __forceinline__ double operator()(int j) const { return __ldg(x + j); }
+    __device__ __forceinline__ double operator()(int j) const { return IBM_XLD(x + j); }
 };
 // x_j = (omega d_j) * b_j  — the damped-Jacobi pre-smoothed iterate of amg.hpp:210 computed on the fly
 struct XJacobi {
     const double* wd;
     const double* b;
-    __device__ __forceinline__ double operator()(int j) const { return mul(__ldg(wd + j), __ldg(b + j)); }
+    __device__ __forceinline__ double operator()(int j) const { return mul(__ldg(wd + j), IBM_XLD(b + j)); }
 };
 
 // ---------------------------------------------------------------- SpMV kernels
@@ -564,8 +583,17 @@ __global__ void __launch_bounds__(kBlock, IBMGPU_ADAPT_MINB) k_spmv_adapt(AdaptP
         double t[1] = {s};
         block_sum<1>(t);
         if (threadIdx.x == 0) {
+            // The row's share of a fused reduction goes to its own partial slot (gridDim.x + long-row
+            // id), never into this CTA's block partial: which CTA completes a split row depends on
+            // arrival order, so a block slot would make the reduction order (and omega, alpha, ...)
+            // run-dependent. The finalize sums the block slots, then the long-row slots, in order.
+            double racc[NR > 0 ? NR : 1];
+#pragma unroll
+            for (int r = 0; r < (NR > 0 ? NR : 1); ++r) racc[r] = 0.0;
+            bool done_row = false;
             if (lr.y == 1) {
-                epi.row(row, t[0], acc);
+                epi.row(row, t[0], racc);
+                done_row = true;
             } else {
                 pl.lpart[lr.x + chunk] = t[0];
                 __threadfence();
@@ -574,7 +602,15 @@ __global__ void __launch_bounds__(kBlock, IBMGPU_ADAPT_MINB) k_spmv_adapt(AdaptP
                     double tot = 0.0;
                     for (int q = 0; q < lr.y; ++q) tot += __ldcg(pl.lpart + lr.x + q);
                     pl.lcnt[m.w] = 0;
-                    epi.row(row, tot, acc);
+                    epi.row(row, tot, racc);
+                    done_row = true;
+                }
+            }
+            if constexpr (NR > 0) {
+                if (done_row) {
+                    const RedSlot rs = epi.slot();
+#pragma unroll
+                    for (int r = 0; r < NR; ++r) rs.partials[(size_t)(gridDim.x + m.w) * NR + r] = racc[r];
                 }
             }
         }
@@ -684,7 +720,10 @@ inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
         grid = A->n_blocks;
         launch_k(c, k_spmv_adapt<XF, Epi>, grid, kBlock, s, pl, A->rp.p, A->ci.p, A->v.p, xf, epi);
     }
-    if constexpr (Epi::NR > 0) launch_k(c, k_finalize<Epi>, 1, kFinThreads, s, epi, grid);
+    // adaptive plans: the long rows' reduction slots follow the CTAs' (k_spmv_adapt)
+    const int slots = (A->kind == SPMV_SELL || A->kind == SPMV_SELLW || A->kind == SPMV_STENCIL) ? grid
+                                                                                                : grid + A->n_lrows;
+    if constexpr (Epi::NR > 0) launch_k(c, k_finalize<Epi>, 1, kFinThreads, s, epi, slots);
 }
 
 // Number of blocks launch_spmv uses (sizes the reduction partials).
@@ -694,7 +733,7 @@ inline int spmv_grid(const Mat* A) {
     if (A->kind == SPMV_SELLW)
         return (A->n_short + kBlock - 1) / kBlock + (A->n_long + kBlock / 32 - 1) / (kBlock / 32);
     if (A->kind == SPMV_STENCIL) return (A->rows + kBlock - 1) / kBlock;
-    return A->n_blocks;
+    return A->n_blocks + A->n_lrows;  // CTAs + one reduction slot per split long row
 }
 
 // Plain epilogue: y_i = s.

@@ -660,6 +660,8 @@ void amg_solve(Ctx* c, Mat* A, Hier* h, const double* b, double* x, const ibm_so
             }
         }
         const double rel = std::sqrt(hn[1]) / bnorm;
+        static const bool dbg = std::getenv("IBMGPU_DEBUG_AMG") != nullptr;
+        if (dbg && (it < 12 || it % 1000 == 0)) std::fprintf(stderr, "[amg] it %d rel %.6e bb %.6e\n", it, rel, hn[0]);
         R.rel_residual = rel;
         R.iterations = it;
         if (rel <= prm.rel_tol) {

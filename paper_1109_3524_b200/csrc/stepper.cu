@@ -17,6 +17,10 @@
 //   invariants (stepper.hpp:323-345)      Q^T SpMV + fused div/slip/NaN reductions
 // This file is compiled with --fmad=false: every expression rounds like the reference's.
 #include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -419,8 +423,18 @@ __global__ void k_vorticity(int nx, int ny, const double* __restrict__ dx, const
 }
 }  // namespace
 
+namespace ibmgpu {
+struct OpsPipeline;
+void pipeline_free(OpsPipeline* p);
+}  // namespace ibmgpu
+
 struct ibmgpu_stepper {
     Ctx* c = nullptr;
+    // moving bodies: the operators of the next steps (E, Q, Q^T, lhs2 and, on the policy steps, the
+    // SA hierarchy) are prepared ahead on a worker stream — they depend only on the prescribed
+    // kinematics, never on the flow state (stepper.cu OpsPipeline)
+    ibmgpu::OpsPipeline* pipe = nullptr;
+    bool pipe_on = false;
     ibmhost::Case cfg;
     ibmhost::Grid g;
     std::vector<ibmhost::Body> bodies;
@@ -477,6 +491,8 @@ struct ibmgpu_stepper {
     DBuf<double> b2, x2, b1, x1;
 
     ~ibmgpu_stepper() {
+        pipeline_free(pipe);
+        pipe = nullptr;
         if (c) cudaStreamSynchronize(c->stream);
         dist_destroy(dist);
         dist_destroy(dist1);
@@ -775,6 +791,10 @@ void stepper_setup(ibmgpu_stepper* S, const char* path, const ibm_case_overrides
     S->check_refresh = std::getenv("IBMGPU_CHECK_REFRESH") != nullptr;
     if (S->n_b > 0 && S->geom_static_after > 0.0 && !std::getenv("IBMGPU_FULL_REFRESH"))
         S->rcache.init(c, S->G, S->BN, S->lhs2, S->n_p, S->pin, S->n_order);
+    {
+        const char* e = std::getenv("IBMGPU_PIPELINE");  // IBMGPU_PIPELINE=0: operators built in line
+        S->pipe_on = S->rcache.ready() && !(e && e[0] == '0');
+    }
     lap("E, H, Q, Q^T, lhs2");
     for (Mat* m : {S->L, S->A, S->BN, S->G}) mat_plan(c, m);
     lap("SpMV plans");
@@ -853,6 +873,166 @@ void set_err(ibm_step_report* rep, const std::string& m) {
 std::string fmt_res(double r) { return std::to_string(r); }
 
 // Stepper::advance (stepper.hpp:231-356)
+}  // namespace
+
+namespace ibmgpu {
+
+// ---------------------------------------------------------------- operator pipeline
+// refresh_body_operators (operators.hpp:445-450) and the policy rebuilds of build_sa_hierarchy
+// (stepper.hpp:257-265) for the coming steps, computed by a worker thread on its own stream while
+// the main stream runs the current step's solves. Inputs: the prescribed body positions at each
+// step's t_new (the same sequence of t + dt additions as the stepper), G, B^N and the refresh
+// cache — all constant — so every prepared operator is bit-identical to the in-line one; the
+// main thread only installs them. The worker runs at most `depth` steps ahead.
+struct Prepared {
+    int step = -1;
+    double t_new = 0.0;
+    bool moving = false, rebuild = false;
+    std::vector<ibmhost::Body> bodies;  // positions at t_new
+    Mat *E = nullptr, *Q = nullptr, *QT = nullptr, *lhs2 = nullptr;
+    Hier* hier = nullptr;
+    int err_code = 0;
+    std::string err;
+    long long launches = 0;
+    double worker_ms = 0.0;
+    ~Prepared() {
+        for (Mat* m : {E, Q, QT, lhs2}) delete m;
+        delete hier;
+    }
+};
+
+struct OpsPipeline {
+    ibmgpu_stepper* S = nullptr;
+    Ctx wc;  // worker context: own stream, the stepper context's pool
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<std::unique_ptr<Prepared>> ready;
+    int depth = 2;
+    bool stop = false, finished = false;
+    int next_step = 0;   // worker timeline
+    double t_prev = 0.0;
+    std::vector<ibmhost::Body> bodies;
+    DBuf<double> px, py, pds;
+    AggCache agg;
+
+    OpsPipeline(ibmgpu_stepper* st, int step, double t) : S(st), next_step(step), t_prev(t), bodies(st->bodies) {
+        wc.device = S->c->device;
+        wc.num_sms = S->c->num_sms;
+        wc.pool = S->c->pool;
+        wc.eager = S->c->eager;
+        CK(cudaStreamCreateWithFlags(&wc.stream, cudaStreamNonBlocking));
+        CK(cudaStreamSynchronize(S->c->stream));
+        agg = std::move(S->agg_cache);  // the worker owns the aggregate cache while it runs
+        agg.rehome(wc.stream);
+        th = std::thread([this] { run(); });
+    }
+    ~OpsPipeline() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
+        }
+        cv.notify_all();
+        if (th.joinable()) th.join();
+        ready.clear();
+        px.release(), py.release(), pds.release();
+        cudaStreamSynchronize(wc.stream);
+        agg.rehome(S->c->stream);
+        S->agg_cache = std::move(agg);
+        cudaStreamDestroy(wc.stream);
+    }
+
+    std::unique_ptr<Prepared> produce(int step, double tp) {
+        auto P = std::make_unique<Prepared>();
+        const auto t0 = std::chrono::steady_clock::now();
+        P->step = step;
+        P->t_new = tp + S->dt;
+        P->moving = tp < S->geom_static_after;
+        if (!P->moving) return P;
+        for (auto& b : bodies) b.move_to(P->t_new);
+        P->bodies = bodies;
+        Ctx* c = &wc;
+        try {
+            std::vector<double> hx, hy, hds;
+            for (const auto& b : bodies)
+                for (int p = 0; p < b.n(); ++p) {
+                    hx.push_back(b.x[p]);
+                    hy.push_back(b.y[p]);
+                    hds.push_back(b.ds);
+                }
+            const auto& g = S->g;
+            const double uni[4] = {g.uniform_region.x0, g.uniform_region.x1, g.uniform_region.y0, g.uniform_region.y1};
+            check_support(uni, g.h_min, S->n_b, hx.data(), hy.data());
+            const size_t nb = (size_t)std::max(S->n_b, 1);
+            if (px.n != nb) px.alloc(c, nb), py.alloc(c, nb), pds.alloc(c, nb);
+            h2d(c, px.p, hx.data(), hx.size());
+            h2d(c, py.p, hy.data(), hy.size());
+            h2d(c, pds.p, hds.data(), hds.size());
+            assemble_eh_dev(c, *S->gd, S->n_b, px.p, py.p, pds.p, &P->E, nullptr);
+            coupled_refresh(c, S->rcache, S->G, P->E, S->BN, &P->Q, &P->QT, &P->lhs2);
+            for (Mat* m : {P->Q, P->QT, P->lhs2}) mat_plan(c, m);
+            const bool freezing = P->t_new >= S->geom_static_after;
+            P->rebuild = S->force_rebuild || freezing || step % S->n_pc == 0;
+            if (P->rebuild) P->hier = sa_build(c, P->lhs2, S->sa, &agg);
+            sync(c);
+        } catch (const Error& e) {
+            cudaStreamSynchronize(wc.stream);
+            P->err_code = e.code;
+            P->err = e.what();
+        } catch (const std::exception& e) {
+            cudaStreamSynchronize(wc.stream);
+            P->err_code = IBMGPU_ECUDA;
+            P->err = e.what();
+        }
+        P->launches = wc.launches;
+        wc.launches = 0;
+        P->worker_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        return P;
+    }
+
+    void run() {
+        cudaSetDevice(wc.device);
+        for (;;) {
+            int step;
+            double tp;
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return stop || (!finished && (int)ready.size() < depth); });
+                if (stop) return;
+                step = next_step;
+                tp = t_prev;
+            }
+            auto P = produce(step, tp);
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                if (!P->moving || P->err_code) finished = true;
+                t_prev = P->t_new;
+                ++next_step;
+                ready.push_back(std::move(P));
+            }
+            cv.notify_all();
+        }
+    }
+
+    // the prepared operators of `step` (waits for them); nullptr if the pipeline is on another step
+    std::unique_ptr<Prepared> take(int step) {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return !ready.empty(); });
+        if (ready.front()->step != step) return nullptr;
+        auto P = std::move(ready.front());
+        ready.pop_front();
+        lk.unlock();
+        cv.notify_all();
+        return P;
+    }
+};
+
+void pipeline_free(OpsPipeline* p) { delete p; }
+
+}  // namespace ibmgpu
+
+namespace {
+
 // NVTX range per phase of Stepper::advance (stepper.hpp:232-321): visible in any CUDA profiler
 // timeline (nsys / ncu --nvtx); the ranges cover the host enqueue of each phase
 struct NvtxRange {
@@ -871,9 +1051,56 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
     rep->ok = 1;
     const double t_new = S->t + S->dt;
     const bool moving = S->t < S->geom_static_after;
-    for (auto& b : S->bodies) b.move_to(t_new);
     auto tic = clk::now();
-    if (moving) {
+    if (moving && S->pipe_on && S->rcache.ready() && !S->dist && S->dist_ranks == 0 && !c->nccl) {
+        NvtxRange r("install prepared operators");
+        std::unique_ptr<Prepared> P;
+        for (int attempt = 0; attempt < 2 && !P; ++attempt) {
+            if (!S->pipe) S->pipe = new OpsPipeline(S, S->step, S->t);
+            P = S->pipe->take(S->step);
+            if (!P) {  // the pipeline ran on another timeline (a failed step was repeated, a restore)
+                pipeline_free(S->pipe);
+                S->pipe = nullptr;
+            }
+        }
+        require(P != nullptr, "stepper: operator pipeline out of step");
+        if (P->err_code) {
+            pipeline_free(S->pipe);
+            S->pipe = nullptr;
+            if (P->err_code == IBMGPU_ESUPPORT) {
+                set_err(rep, P->err);
+                return;
+            }
+            fail(P->err_code, P->err);
+        }
+        // install: the worker synchronised its stream, so the operators are complete; their
+        // buffers are handed to the main stream
+        for (Mat* m : {P->E, P->Q, P->QT, P->lhs2}) mat_rehome(m, c->stream);
+        pcg_forget(c, S->lhs2, nullptr);
+        delete S->E;
+        delete S->H;
+        delete S->Q;
+        delete S->QT;
+        delete S->lhs2;
+        S->E = P->E, S->H = nullptr, S->Q = P->Q, S->QT = P->QT, S->lhs2 = P->lhs2;
+        P->E = P->Q = P->QT = P->lhs2 = nullptr;
+        S->bodies = P->bodies;
+        S->upload_bodies();
+        S->dist_stale = true;
+        c->launches += P->launches;
+        rep->rebuilt_operators = 1;
+        if (P->rebuild) {
+            hier_rehome(P->hier, c->stream);
+            pcg_forget(c, nullptr, S->hier);
+            delete S->hier;
+            S->hier = P->hier;
+            P->hier = nullptr;
+            S->hier->built_at_step = S->step;
+            rep->rebuilt_hierarchy = 1;
+        }
+        rep->t_assembly = std::chrono::duration<double>(clk::now() - tic).count();  // wait + install
+    } else if (moving) {
+        for (auto& b : S->bodies) b.move_to(t_new);
         try {
             NvtxRange r("refresh_body_operators");
             S->refresh_body_operators();
@@ -897,6 +1124,7 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
             rep->t_precond = std::chrono::duration<double>(clk::now() - tic).count();
         }
     } else if (S->n_b) {
+        for (auto& b : S->bodies) b.move_to(t_new);
         // geometry fixed, velocities may still change (e.g. rotating circle): refresh u_B only
         S->upload_bodies();
     }
@@ -1264,6 +1492,8 @@ int ibmgpu_stepper_set(ibmgpu_stepper_t S, int which, const double* in, int n) {
             case 3: dst = S->bnd.p, len = S->bl.total; break;
             case 4: {
                 require(n == 3, "stepper_set: scalars expect t, step, have_conv");
+                pipeline_free(S->pipe);  // its timeline starts from the old state
+                S->pipe = nullptr;
                 S->t = in[0];
                 S->step = (int)in[1];
                 S->have_conv = in[2] != 0.0;
@@ -1362,6 +1592,8 @@ int ibmgpu_stepper_distribute(ibmgpu_stepper_t S, int virtual_ranks, int min_dis
     return sguard(S, [&] {
         require(virtual_ranks >= 0, "stepper_distribute: virtual_ranks must be >= 0");
         require(!S->multi_rank() || virtual_ranks <= 1, "stepper_distribute: virtual ranks need a single-rank context");
+        pipeline_free(S->pipe);  // distributed steps build their operators in line
+        S->pipe = nullptr;
         S->dist_ranks = S->multi_rank() ? S->c->nranks : virtual_ranks;
         S->dist_min_rows = min_dist_rows;
         S->dist_stale = true;
