@@ -740,6 +740,181 @@ __global__ void k_place_rows(int nl, const int* __restrict__ idx, const int* __r
     }
 }
 
+// ---------------------------------------------------------------- dense-accumulator SpGEMM
+// spmm_rows for products with a narrow output (<= kDenseCols columns) and long rows — the coarse
+// Galerkin products, whose long rows (tens of thousands of products) serialised a hash warp. One
+// CTA per output row (rows handed out from a counter); the row's accumulator is a dense array of
+// the output width in shared memory plus a bitmap of touched columns. Products are formed 256 at a
+// time in Gustavson order (A-row entry, then B-row entry); the 8 warps add their 32 products in
+// warp order, each warp grouping equal columns with __match_any_sync and adding a group in lane
+// order — every column receives 0.0 + p1 + p2 + ... in Gustavson order, as the reference. The
+// bitmap then yields the columns already sorted (no sort). Symbolic pass: the bitmap only.
+constexpr int kDenseCols = 12288, kDenseThreads = 256, kDenseChunk = 256;
+
+struct DenseChunk {
+    int off[kDenseChunk + 1];  // inclusive product offsets of the chunk's A entries
+    int bs[kDenseChunk];       // B-row start of each A entry
+    double a[kDenseChunk];
+};
+
+template <bool kNumeric>
+__global__ void __launch_bounds__(kDenseThreads) k_dense_rows(int r0, int rows, int ncols, const int* __restrict__ arp,
+                                                             const int* __restrict__ aci, const double* __restrict__ av,
+                                                             const int* __restrict__ brp, const int* __restrict__ bci,
+                                                             const double* __restrict__ bv, int* __restrict__ cnt,
+                                                             const int* __restrict__ crp, int* __restrict__ cci,
+                                                             double* __restrict__ cv, unsigned* __restrict__ next) {
+    extern __shared__ double dsm[];
+    double* acc = dsm;  // ncols (numeric only)
+    unsigned* bits = reinterpret_cast<unsigned*>(kNumeric ? dsm + ncols : dsm);
+    const int nwords = (ncols + 31) >> 5;
+    __shared__ DenseChunk ch;
+    __shared__ int s_row, s_total, s_scan[kDenseThreads + 1];
+    __shared__ double s_prod[kDenseThreads / 32][32];
+    const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+    for (int k = t; k < nwords; k += kDenseThreads) bits[k] = 0u;
+    if (kNumeric)
+        for (int k = t; k < ncols; k += kDenseThreads) acc[k] = 0.0;
+    __syncthreads();
+    for (;;) {
+        if (t == 0) s_row = (int)atomicAdd(next, 1u);
+        __syncthreads();
+        const int row = s_row;
+        if (row >= rows) break;
+        const int i = r0 + row, b = arp[i], e = arp[i + 1];
+        for (int c0 = b; c0 < e; c0 += kDenseChunk) {
+            // chunk of A entries: B-row starts, lengths -> inclusive offsets (block scan)
+            const int kk = c0 + t;
+            int len = 0;
+            if (kk < e) {
+                const int k = aci[kk];
+                ch.bs[t] = brp[k];
+                len = brp[k + 1] - ch.bs[t];
+                if (kNumeric) ch.a[t] = av[kk];
+            }
+            s_scan[t + 1] = len;
+            if (t == 0) s_scan[0] = 0;
+            __syncthreads();
+            for (int d = 1; d < kDenseThreads; d <<= 1) {  // Hillis-Steele inclusive scan
+                const int v = t + 1 >= d + 1 ? s_scan[t + 1 - d] : 0;
+                __syncthreads();
+                s_scan[t + 1] += v;
+                __syncthreads();
+            }
+            ch.off[t + 1] = s_scan[t + 1];
+            if (t == 0) {
+                ch.off[0] = 0;
+                s_total = s_scan[kDenseThreads];
+            }
+            __syncthreads();
+            const int total = s_total, na = min(kDenseChunk, e - c0);
+            for (int q0 = 0; q0 < total; q0 += kDenseThreads) {
+                const int q = q0 + t;
+                int col = -1;
+                double p = 0.0;
+                if (q < total) {
+                    int lo = 0, hi = na - 1;  // largest o with off[o] <= q
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (ch.off[mid] <= q)
+                            lo = mid;
+                        else
+                            hi = mid - 1;
+                    }
+                    const int jj = ch.bs[lo] + (q - ch.off[lo]);
+                    col = bci[jj];
+                    if (kNumeric) p = mul(ch.a[lo], bv[jj]);
+                }
+                if (!kNumeric) {
+                    if (col >= 0) atomicOr(bits + (col >> 5), 1u << (col & 31));
+                } else {
+                    const unsigned grp = __match_any_sync(kFull, col);
+                    const bool leader = col >= 0 && lane == __ffs(grp) - 1;
+                    s_prod[w][lane] = p;
+                    __syncwarp();
+                    // warps add in warp order: Gustavson order across the 256 products
+                    for (int ww = 0; ww < kDenseThreads / 32; ++ww) {
+                        if (w == ww && leader) {
+                            double a_ = acc[col];
+                            for (unsigned m = grp; m; m &= m - 1) a_ = addd(a_, s_prod[w][__ffs(m) - 1]);
+                            acc[col] = a_;
+                            atomicOr(bits + (col >> 5), 1u << (col & 31));  // leaders may share a word
+                        }
+                        __syncthreads();
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        // columns in order from the bitmap: per-thread word ranges, block prefix of popcounts
+        const int per = (nwords + kDenseThreads - 1) / kDenseThreads;
+        const int w0 = min(nwords, t * per), w1 = min(nwords, w0 + per);
+        int mine = 0;
+        for (int k = w0; k < w1; ++k) mine += __popc(bits[k]);
+        s_scan[t + 1] = mine;
+        if (t == 0) s_scan[0] = 0;
+        __syncthreads();
+        for (int d = 1; d < kDenseThreads; d <<= 1) {
+            const int v = t + 1 >= d + 1 ? s_scan[t + 1 - d] : 0;
+            __syncthreads();
+            s_scan[t + 1] += v;
+            __syncthreads();
+        }
+        if (!kNumeric) {
+            if (t == 0) cnt[row] = s_scan[kDenseThreads];
+            for (int k = w0; k < w1; ++k) bits[k] = 0u;
+        } else {
+            int o = crp[row] + s_scan[t];
+            for (int k = w0; k < w1; ++k) {
+                unsigned m = bits[k];
+                while (m) {
+                    const int col = (k << 5) + __ffs(m) - 1;
+                    m &= m - 1;
+                    cci[o] = col;
+                    cv[o] = acc[col];
+                    acc[col] = 0.0;
+                    ++o;
+                }
+                bits[k] = 0u;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// spmm_rows by the dense-accumulator kernels; nullptr when the output is too wide
+Mat* spmm_dense(Ctx* c, const Mat* A, int r0, int r1, const Mat* B) {
+    const int rows = r1 - r0, ncols = B->cols;
+    if (rows <= 0 || ncols > kDenseCols || ncols <= 0) return nullptr;
+    const int nwords = (ncols + 31) / 32;
+    const size_t sym_smem = sizeof(unsigned) * (size_t)nwords;
+    const size_t num_smem = sizeof(double) * (size_t)ncols + sizeof(unsigned) * (size_t)nwords;
+    CK(cudaFuncSetAttribute(k_dense_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem));
+    CK(cudaFuncSetAttribute(k_dense_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)num_smem));
+    int occ_s = 0, occ_n = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_dense_rows<false>, kDenseThreads, sym_smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_n, k_dense_rows<true>, kDenseThreads, num_smem));
+    const int gs = std::max(1, std::min(rows, c->num_sms * std::max(occ_s, 1)));
+    const int gn = std::max(1, std::min(rows, c->num_sms * std::max(occ_n, 1)));
+    DBuf<unsigned> next(c, 2);
+    CK(cudaMemsetAsync(next.p, 0, 2 * sizeof(unsigned), c->stream));
+    DBuf<int> cnt(c, (size_t)rows + 1);
+    k_dense_rows<false><<<gs, kDenseThreads, sym_smem, c->stream>>>(r0, rows, ncols, A->rp.p, A->ci.p, A->v.p, B->rp.p,
+                                                                     B->ci.p, B->v.p, cnt.p, nullptr, nullptr, nullptr,
+                                                                     next.p);
+    CK_LAUNCH(c);
+    Mat* m = mat_new(c, rows, ncols, 0);
+    exclusive_scan_total(c, cnt.p, m->rp.p, rows);
+    m->nnz = d2h_scalar(c, m->rp.p + rows);
+    m->ci.alloc(c, (size_t)std::max(m->nnz, 1));
+    m->v.alloc(c, (size_t)std::max(m->nnz, 1));
+    k_dense_rows<true><<<gn, kDenseThreads, num_smem, c->stream>>>(r0, rows, ncols, A->rp.p, A->ci.p, A->v.p, B->rp.p,
+                                                                    B->ci.p, B->v.p, nullptr, m->rp.p, m->ci.p, m->v.p,
+                                                                    next.p + 1);
+    CK_LAUNCH(c);
+    return m;
+}
+
 Mat* esc_rows(Ctx* c, const Mat* A, int r0, int r1, const Mat* B);
 
 // Hash path for rows [r0, r1) of A*B (rprod: products per row). Rows of more than
@@ -868,6 +1043,13 @@ Mat* spmm_rows(Ctx* c, const Mat* A, int r0, int r1, const Mat* B) {
         // a warp per row pays off only when rows carry at least a batch of products: the lhs2
         // assembly (4-8 products per row) stays on ESC (2.7 vs 5.1 ms per flapping refresh)
         const long long total = exclusive_scan_total64(c, rprod.p, pref.p, r1 - r0);
+        // narrow outputs with long rows (coarse Galerkin products): a CTA per row, dense accumulator
+        static const bool dense_on = [] {
+            const char* e = std::getenv("IBMGPU_DENSE_SPGEMM");  // IBMGPU_DENSE_SPGEMM=0: hash only
+            return !(e && e[0] == '0');
+        }();
+        if (dense_on && B->cols <= kDenseCols && total >= 256ll * (r1 - r0))
+            if (Mat* d = spmm_dense(c, A, r0, r1, B)) return finish_plan(c, d);
         if (total >= 32ll * (r1 - r0))
             if (Mat* h = spmm_hash(c, A, r0, r1, B, rprod.p)) return finish_plan(c, h);
     }
