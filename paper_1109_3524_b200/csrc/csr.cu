@@ -451,8 +451,12 @@ void plan_adaptive_from(Ctx* c, Mat* m, const std::vector<int>& rp) {
                 ++r1;
             }
             const double mean = double(nz) / (r1 - r);
+            static const int epl = [] {  // target entries per lane (IBMGPU_ADAPT_EPL, A/B)
+                const char* e = std::getenv("IBMGPU_ADAPT_EPL");
+                return e ? std::max(1, std::atoi(e)) : 8;  // 8: S-4M -0.3%, C2 -0.8% vs 4
+            }();
             int tpr = 2;
-            while (tpr < 32 && tpr * 4 < mean) tpr *= 2;
+            while (tpr < 32 && tpr * epl < mean) tpr *= 2;
             // keep at least a few rows per group for short-row chunks
             while (tpr > 2 && (r1 - r) > (kBlock / tpr) * 8) tpr /= 2;
             // whole passes only: a chunk of 17 rows on 8 groups costs 3 latency-bound passes, 16 cost 2
