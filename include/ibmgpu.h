@@ -149,6 +149,11 @@ int ibmgpu_hier_info(ibmgpu_hier_t h, int* n_levels, int* stalled, int* coarse_r
 /* device-only (no reference counterpart): how many of the last levels the V-cycle applies as one
  * folded dense operator, and its dimension (0 and coarse_rows when nothing is folded; fold.cu) */
 int ibmgpu_hier_folded(ibmgpu_hier_t h, int* n_fold, int* dense_rows);
+/* device-only: the level-0 grid transfers applied through the pressure stencil (xfer.cuh) instead
+ * of streaming the explicit P and P^T — the same operator as amg.hpp:163-183, rounded differently.
+ * mode 0 turns them off, 1 on (if level 0 qualifies), -1 only queries; *active gets the state.
+ * PCG plans capture the state when they are made. */
+int ibmgpu_hier_transfers(ibmgpu_ctx_t ctx, ibmgpu_hier_t h, int mode, int* active);
 /* level l: borrowed handles (valid while h lives) and omega; l == n_levels gives coarse_A in *A */
 int ibmgpu_hier_level(ibmgpu_hier_t h, int l, ibmgpu_mat_t* A, ibmgpu_mat_t* P, ibmgpu_mat_t* Pt, double* omega);
 /* aggregate ids of level l's core rows (sa_detail::aggregate, amg.hpp:79-107); returns count */

@@ -123,6 +123,7 @@ _SIGS = [
     ("ibmgpu_amg_solve", C.c_int, [_vp, _vp, _vp, _dp, _dp, C.POINTER(SolverParamsC), C.POINTER(SolveResultC)]),
     ("ibmgpu_hier_info", C.c_int, [_vp, _ip, _ip, _ip]),
     ("ibmgpu_hier_folded", C.c_int, [_vp, _ip, _ip]),
+    ("ibmgpu_hier_transfers", C.c_int, [_vp, _vp, C.c_int, _ip]),
     ("ibmgpu_hier_level", C.c_int, [_vp, C.c_int, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _dp]),
     ("ibmgpu_hier_aggregates", C.c_int, [_vp, _vp, C.c_int, _ip, _ip]),
     ("ibmgpu_aggregate", C.c_int, [_vp, _vp, C.c_double, C.c_int, _ip, _ip]),

@@ -19,6 +19,7 @@
 #include "coarse.cuh"
 #include "internal.cuh"
 #include "kern.cuh"
+#include "xfer.cuh"
 
 struct ibmgpu_hier;
 
@@ -41,6 +42,15 @@ struct Level {
     }
 };
 
+// Level-0 transfers through the stencil (xfer.cuh / xfer.cu); on = false: the explicit P / P^T
+struct Xfer0 {
+    bool on = false;
+    bool built = false;  // plan and buffers exist (on may be switched off and back)
+    int S = 0, NY = 0, n_ti = 0, tiles = 0, tail_ctas = 0;
+    DBuf<double> tagg, r1t;
+    DBuf<int> mrp, mem;
+};
+
 }  // namespace ibmgpu
 
 struct ibmgpu_hier {
@@ -60,6 +70,7 @@ struct ibmgpu_hier {
     int n_phases = 0, coarse_grid = 0;
     ibmgpu::DBuf<ibmgpu::Phase> phases;
     ibmgpu::DBuf<unsigned> bar;       // {count, generation}
+    ibmgpu::Xfer0 x0;
     bool stalled = false;
     long long id = 0;
     int built_at_step = -1;
@@ -83,6 +94,7 @@ inline void hier_rehome(Hier* h, cudaStream_t s) {
     if (h->coarse_A) mat_rehome(h->coarse_A, s);
     set(h->coarse_inv), set(h->coarse_tiles), set(h->prow), set(h->pcol), set(h->cb), set(h->cx), set(h->dense);
     set(h->phases), set(h->bar);
+    set(h->x0.tagg), set(h->x0.r1t), set(h->x0.mrp), set(h->x0.mem);
 }
 
 // Aggregates of the previous build, per level, keyed by the strength graph they came from.
@@ -102,6 +114,17 @@ struct AggCache {
                 if (b->p) b->s = s;
     }
 };
+
+// xfer.cu
+bool xfer0_enabled();
+void xfer0_setup(Ctx* c, Hier* h);
+inline XferPlan xfer_plan(const Hier* h) {
+    const Level& lv = *h->levels[0];
+    const Mat* A = lv.A;
+    return XferPlan{StencilPlan{A->st_v.p, A->st_mask.p, A->st_erp.p, A->st_eci.p, A->st_ev.p, A->st_S1, A->st_S2},
+                    A->rows, lv.n_core, h->x0.S, h->x0.NY, lv.n_agg, h->x0.n_ti, h->x0.tiles, h->x0.tail_ctas,
+                    lv.x.p, lv.wd.p, lv.agg.p, h->x0.tagg.p, h->x0.mrp.p, h->x0.mem.p};
+}
 
 // amg_setup.cu
 Hier* sa_build(Ctx* c, const Mat* A, const ibm_sa_options& o, AggCache* cache = nullptr);
@@ -246,6 +269,21 @@ inline void vcycle_launch(Ctx* c, Hier* h, const double* r_in, double* z_out, co
     for (int l = 0; l < F; ++l) {
         Level& lv = *h->levels[l];
         const double* b = l == 0 ? r_in : lv.b.p;
+        if (l == 0 && h->x0.on) {  // stencil transfers (xfer.cuh): s into lv.r, then b_1 = P^T r1
+            const XferPlan X = xfer_plan(h);
+            launch_k(c, k_xfer_down, h->x0.tail_ctas + h->x0.tiles, kBlock, s, X, b, lv.r.p, h->x0.r1t.p, done);
+            const int n1 = l + 1 < L ? h->levels[1]->A->rows : h->n_dense;
+            const int g = (n1 + kBlock - 1) / kBlock;
+            if (l + 1 < L) {
+                Level& nx = *h->levels[1];
+                launch_k(c, k_xfer_restrict, g, kBlock, s, X, n1, (const double*)lv.r.p, (const double*)h->x0.r1t.p,
+                         nx.b.p, (const double*)nx.wd.p, nx.xj.p, done);
+            } else {
+                launch_k(c, k_xfer_restrict, g, kBlock, s, X, n1, (const double*)lv.r.p, (const double*)h->x0.r1t.p,
+                         h->cb.p, (const double*)nullptr, (double*)nullptr, done);
+            }
+            continue;
+        }
         // level 0 forms x_j = (w d)_j r_j inside the gather; deeper levels gather the iterate the
         // restriction above already wrote (one gather per entry instead of two)
         if (l == 0)
@@ -271,6 +309,10 @@ inline void vcycle_launch(Ctx* c, Hier* h, const double* r_in, double* z_out, co
         Level& lv = *h->levels[l];
         const double* b = l == 0 ? r_in : lv.b.p;
         const double* ec = l + 1 < L ? h->levels[l + 1]->xo.p : h->cx.p;
+        if (l == 0 && h->x0.on) {
+            last.xfer(h, b, ec, z_out);
+            continue;
+        }
         launch_spmv(c, lv.P, XPlain{ec}, EpiAddInPlace{lv.x.p, done}, s);
         if (l > 0) {
             launch_spmv(c, lv.A, XPlain{lv.x.p}, EpiPostSmooth{lv.wd.p, b, lv.x.p, lv.xo.p, done}, s);
@@ -288,13 +330,19 @@ struct LastPlain {
     void operator()(Level& lv, const double* b, double* z) const {
         launch_spmv(c, lv.A, XPlain{lv.x.p}, EpiPostSmooth{lv.wd.p, b, lv.x.p, z, done}, s);
     }
+    void xfer(Hier* h, const double* b, const double* e, double* z) const {
+        const XSinkPlain sink{z, done};
+        launch_k(c, k_xfer_up<XSinkPlain>, h->x0.tiles, kBlock, s, xfer_plan(h), b, e, sink);
+        if (h->x0.tail_ctas)
+            launch_k(c, k_xfer_up_tail<XSinkPlain>, h->x0.tail_ctas, kBlock, s, xfer_plan(h), b, e, sink, h->x0.tiles);
+    }
 };
 
 // kernels launched by one V-cycle (for launch accounting)
 inline int vcycle_kernels(const Hier* h) {
     if (h->levels.empty()) return 1;
     const int F = h->n_phases ? h->fuse_from : h->active_levels();
-    return 4 * F + 2;  // + the two SYMV kernels
+    return 4 * F + 2 - (h->x0.on && !h->x0.tail_ctas ? 1 : 0);  // + the two SYMV kernels
 }
 
 }  // namespace ibmgpu

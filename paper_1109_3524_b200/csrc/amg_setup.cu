@@ -1174,6 +1174,8 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o, AggCache* cac
         } else {
             build_fused_coarse(c, h);
         }
+        xfer0_setup(c, h);
+        clk.lap("xfer0", -1);
         sync(c);
     } catch (...) {
         delete h;

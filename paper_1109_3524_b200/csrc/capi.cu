@@ -370,6 +370,15 @@ int ibmgpu_hier_folded(ibmgpu_hier_t h, int* n_fold, int* dense_rows) {
     return 0;
 }
 
+int ibmgpu_hier_transfers(ibmgpu_ctx_t c, ibmgpu_hier_t h, int mode, int* active) {
+    return guard(c, [&] {
+        need(h != nullptr, "hier_transfers: null hierarchy");
+        if (mode == 0) h->x0.on = false;
+        if (mode == 1 && !h->x0.on) xfer0_setup(c, h);
+        if (active) *active = h->x0.on ? 1 : 0;
+    });
+}
+
 int ibmgpu_hier_level(ibmgpu_hier_t h, int l, ibmgpu_mat_t* A, ibmgpu_mat_t* P, ibmgpu_mat_t* Pt, double* omega) {
     if (!h || l < 0 || l > (int)h->levels.size()) return IBMGPU_EINVAL;
     if (l == (int)h->levels.size()) {

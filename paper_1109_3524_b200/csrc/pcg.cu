@@ -229,6 +229,14 @@ struct LastDot {
     void operator()(Level& lv, const double* b, double* z) const {
         launch_spmv(c, lv.A, XPlain{lv.x.p}, EpiPostSmoothDot<Fin>{lv.wd.p, b, lv.x.p, z, done, rs, f}, s);
     }
+    void xfer(Hier* h, const double* b, const double* e, double* z) const {
+        const XSinkDot<Fin> sink{z, done, rs, f};
+        const XferPlan X = xfer_plan(h);
+        launch_k(c, k_xfer_up<XSinkDot<Fin>>, h->x0.tiles, kBlock, s, X, b, e, sink);
+        if (h->x0.tail_ctas)
+            launch_k(c, k_xfer_up_tail<XSinkDot<Fin>>, h->x0.tail_ctas, kBlock, s, X, b, e, sink, h->x0.tiles);
+        launch_k(c, k_finalize<XSinkDot<Fin>>, 1, kFinThreads, s, sink, h->x0.tiles + h->x0.tail_ctas);
+    }
 };
 
 template <class Fin>
@@ -276,6 +284,7 @@ PcgPlan::PcgPlan(Ctx* c, Mat* A_, int kind_, Hier* h_) : A(A_), kind(kind_), h(h
     int g = std::max(spmv_grid(A), elem_grid(c, (long long)n));
     if (h)
         for (auto& lv : h->levels) g = std::max(g, spmv_grid(lv->A));
+    if (h && h->x0.on) g = std::max(g, h->x0.tiles + h->x0.tail_ctas);
     partials.alloc(c, (size_t)std::max(g, 1) * 2);
     counter.alloc(c, 1);
     CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), c->stream));

@@ -350,6 +350,12 @@ class SaHierarchy:
         self.ctx.check(self.ctx.lib.ibmgpu_hier_folded(self.h, C.byref(nf), C.byref(nd)))
         return nf.value, nd.value
 
+    def transfers(self, mode: int = -1) -> bool:
+        """Level-0 P / P^T applied through the stencil (xfer.cuh): mode 0 off, 1 on, -1 query."""
+        on = C.c_int()
+        self.ctx.check(self.ctx.lib.ibmgpu_hier_transfers(self.ctx.h, self.h, mode, C.byref(on)))
+        return bool(on.value)
+
     @property
     def n_levels(self) -> int:
         return self.info()[0]
