@@ -36,7 +36,7 @@
 namespace ibmgpu {
 
 constexpr int kXOut = 28;        // output columns per tile (lanes 2..29)
-constexpr int kXTJ = 14;         // output lines per tile
+constexpr int kXTJ = 22;         // output lines per tile
 constexpr int kXL1 = kXTJ + 2;   // band lines (tile + 1): 4 per warp
 constexpr int kXL2 = kXTJ + 4;   // x / y frame lines (tile + 2)
 constexpr int kXK1 = kXL1 / 8;   // band lines per warp
@@ -94,7 +94,7 @@ __device__ __forceinline__ double shup(double v) { return __shfl_up_sync(kFull, 
 __device__ __forceinline__ double shdn(double v) { return __shfl_down_sync(kFull, v, 1); }  // lane + 1
 
 // K_D: s = r1 - A^T(wd r1) on core rows, r1 = b - A (wd b); r1 of the tail rows into r1t.
-static __global__ void __launch_bounds__(kBlock, 4) k_xfer_down(XferPlan X, const double* b, double* s_out,
+static __global__ void __launch_bounds__(kBlock, 3) k_xfer_down(XferPlan X, const double* b, double* s_out,
                                                                 double* r1t, const int* done) {
     __shared__ double sx[kXL2][32];  // x = wd b, frame lines j0-2 ..
     __shared__ double sq4[kXL1][32];  // A_{m,+S} u_m (read by the line below)
@@ -266,7 +266,7 @@ struct XSinkDot {
 
 // K_U: z = x + wd (b - A x), x = wd b + P e, with P e applied through the stencil (see top).
 template <class Sink>
-__global__ void __launch_bounds__(kBlock, 4) k_xfer_up(XferPlan X, const double* b, const double* e, Sink sink) {
+__global__ void __launch_bounds__(kBlock, 3) k_xfer_up(XferPlan X, const double* b, const double* e, Sink sink) {
     __shared__ double sy[kXL2][32];  // y = T e, frame lines j0-2 ..
     __shared__ double sx[kXL1][32];  // x, band lines j0-1 ..
     constexpr int NR = Sink::NR;
