@@ -827,13 +827,14 @@ int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& 
     const bool use_chunk = pick.rfind("chunk", 0) == 0 ? chunk_ok : pick.empty() ? chunk_ok && n_core <= kChunkMax : false;
     if (use_chunk) {
         const size_t smem = chunk_smem(n_core, cap);
+        IBM_SMEM_OPTIN(c, k_greedy_chunk<true>);
+        IBM_SMEM_OPTIN(c, k_greedy_chunk<false>);
         auto kern = lane ? k_greedy_chunk<true> : k_greedy_chunk<false>;
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<1, kChunk, smem, c->stream>>>(n_core, S.rp.p, S.ci.p, status.p, cap);
         CK_LAUNCH(c);
     } else if (pick == "seq") {
         const size_t smem = sizeof(unsigned) * (size_t)((n_core + 31) / 32) + sizeof(int) * (kGD * kGW + kWin + kGD + 1);
-        CK(cudaFuncSetAttribute(k_greedy_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        IBM_SMEM_OPTIN(c, k_greedy_seq);
         k_greedy_seq<<<1, 32, smem, c->stream>>>(n_core, S.rp.p, S.ci.p, status.p);
         CK_LAUNCH(c);
     } else {

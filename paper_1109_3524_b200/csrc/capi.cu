@@ -54,7 +54,11 @@ int ibmgpu_init(int device, int nranks, int rank, const void* nccl_id, ibmgpu_ct
         c->nranks = nranks;
         c->rank = rank;
         CK(cudaSetDevice(device));
-        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        // the solve stream at the highest priority: the stepper's operator-pipeline workers (lowest
+        // priority streams) then fill only the SMs the solves leave idle
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, hi));
         CK(cudaEventCreate(&c->t0));
         CK(cudaEventCreate(&c->t1));
         CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -117,6 +118,25 @@ inline void d2d(Ctx* c, T* dst, const T* src, size_t n) {
     if (n) CK(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyDeviceToDevice, c->stream));
 }
 inline void sync(Ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
+
+// A kernel's dynamic shared-memory limit, raised once to the device's opt-in maximum (minus its
+// static shared memory). Setting it per launch to that launch's size races when two host threads
+// (the stepper's operator-pipeline workers) launch the same kernel with different sizes.
+template <class K>
+inline void smem_optin_once(std::once_flag& f, K kernel, int device) {
+    std::call_once(f, [&] {
+        int mx = 0;
+        CK(cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        cudaFuncAttributes fa{};
+        CK(cudaFuncGetAttributes(&fa, kernel));
+        CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx - (int)fa.sharedSizeBytes));
+    });
+}
+#define IBM_SMEM_OPTIN(c, kernel)                                 \
+    do {                                                          \
+        static std::once_flag ibm_smem_flag_;                     \
+        ::ibmgpu::smem_optin_once(ibm_smem_flag_, kernel, (c)->device); \
+    } while (0)
 
 template <class T>
 inline T d2h_scalar(Ctx* c, const T* src) {

@@ -889,8 +889,8 @@ Mat* spmm_dense(Ctx* c, const Mat* A, int r0, int r1, const Mat* B) {
     const int nwords = (ncols + 31) / 32;
     const size_t sym_smem = sizeof(unsigned) * (size_t)nwords;
     const size_t num_smem = sizeof(double) * (size_t)ncols + sizeof(unsigned) * (size_t)nwords;
-    CK(cudaFuncSetAttribute(k_dense_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem));
-    CK(cudaFuncSetAttribute(k_dense_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)num_smem));
+    IBM_SMEM_OPTIN(c, k_dense_rows<false>);
+    IBM_SMEM_OPTIN(c, k_dense_rows<true>);
     int occ_s = 0, occ_n = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k_dense_rows<false>, kDenseThreads, sym_smem));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_n, k_dense_rows<true>, kDenseThreads, num_smem));
@@ -968,7 +968,7 @@ Mat* spmm_hash(Ctx* c, const Mat* A, int r0, int r1, const Mat* B, const long lo
     lap("long/ESC", nl);
     std::unique_ptr<Mat> hold(Cl);
     const size_t sym_smem = sizeof(int) * (size_t)kSymWarps * kHashSym;
-    CK(cudaFuncSetAttribute(k_hash_symbolic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sym_smem));
+    IBM_SMEM_OPTIN(c, k_hash_symbolic);
     int sym_occ = 0;  // persistent grid: every CTA resident, rows handed out dynamically
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&sym_occ, k_hash_symbolic, kSymWarps * 32, sym_smem));
     const int sgrid = std::min((rows + kSymWarps - 1) / kSymWarps, c->num_sms * std::max(sym_occ, 1));
@@ -990,7 +990,7 @@ Mat* spmm_hash(Ctx* c, const Mat* A, int r0, int r1, const Mat* B, const long lo
     m->nnz = d2h_scalar(c, m->rp.p + rows);
     m->ci.alloc(c, (size_t)std::max(m->nnz, 1));
     m->v.alloc(c, (size_t)std::max(m->nnz, 1));
-    CK(cudaFuncSetAttribute(k_hash_numeric, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    IBM_SMEM_OPTIN(c, k_hash_numeric);
     int num_occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&num_occ, k_hash_numeric, nw * 32, smem));
     const int ngrid = std::min((rows + nw - 1) / nw, c->num_sms * std::max(num_occ, 1));

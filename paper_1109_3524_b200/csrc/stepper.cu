@@ -19,6 +19,8 @@
 #include <chrono>
 #include <condition_variable>
 #include <deque>
+#include <climits>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <cmath>
@@ -901,31 +903,63 @@ struct Prepared {
     }
 };
 
+// Workers build the operators of the next steps concurrently: each owns a stream, an aggregate
+// cache and its body positions, and claims the next unclaimed step (rebuild steps and cheap
+// refresh-only steps interleave, so two workers overlap two hierarchy builds). A build is a chain
+// of small, latency-bound kernels with host round trips, so concurrent builds share the GPU
+// well. IBMGPU_PIPE_WORKERS sets the count (default 2).
 struct OpsPipeline {
+    struct Worker {
+        Ctx wc;  // own stream, the stepper context's pool
+        std::thread th;
+        std::vector<ibmhost::Body> bodies;
+        DBuf<double> px, py, pds;
+        AggCache agg;
+    };
     ibmgpu_stepper* S = nullptr;
-    Ctx wc;  // worker context: own stream, the stepper context's pool
-    std::thread th;
+    std::vector<std::unique_ptr<Worker>> workers;
     std::mutex mu;
     std::condition_variable cv;
-    std::deque<std::unique_ptr<Prepared>> ready;
-    int depth = 2;
-    bool stop = false, finished = false;
-    int next_step = 0;   // worker timeline
-    double t_prev = 0.0;
-    std::vector<ibmhost::Body> bodies;
-    DBuf<double> px, py, pds;
-    AggCache agg;
+    std::map<int, std::unique_ptr<Prepared>> ready;
+    int depth = 2;            // prepared steps ahead per worker
+    int first_step = 0;
+    int next_step = 0;        // next step to claim
+    double t_prev = 0.0;      // time before next_step
+    int in_flight = 0;
+    int finish_step = INT_MAX;  // first step that was not moving (or failed): nothing after it
+    bool stop = false;
 
-    OpsPipeline(ibmgpu_stepper* st, int step, double t) : S(st), next_step(step), t_prev(t), bodies(st->bodies) {
-        wc.device = S->c->device;
-        wc.num_sms = S->c->num_sms;
-        wc.pool = S->c->pool;
-        wc.eager = S->c->eager;
-        CK(cudaStreamCreateWithFlags(&wc.stream, cudaStreamNonBlocking));
+    static int worker_count() {
+        static const int n = [] {
+            const char* e = std::getenv("IBMGPU_PIPE_WORKERS");
+            return e ? std::max(1, std::min(4, std::atoi(e))) : 2;
+        }();
+        return n;
+    }
+
+    OpsPipeline(ibmgpu_stepper* st, int step, double t) : S(st), first_step(step), next_step(step), t_prev(t) {
         CK(cudaStreamSynchronize(S->c->stream));
-        agg = std::move(S->agg_cache);  // the worker owns the aggregate cache while it runs
-        agg.rehome(wc.stream);
-        th = std::thread([this] { run(); });
+        const int nw = worker_count();
+        for (int w = 0; w < nw; ++w) {
+            auto W = std::make_unique<Worker>();
+            W->wc.device = S->c->device;
+            W->wc.num_sms = S->c->num_sms;
+            W->wc.pool = S->c->pool;
+            W->wc.eager = S->c->eager;
+            int lo = 0, hi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CK(cudaStreamCreateWithPriority(&W->wc.stream, cudaStreamNonBlocking, lo));
+            W->bodies = S->bodies;
+            if (w == 0) {
+                W->agg = std::move(S->agg_cache);  // worker 0 owns the stepper's aggregate cache
+                W->agg.rehome(W->wc.stream);
+            }
+            workers.push_back(std::move(W));
+        }
+        for (auto& W : workers) {
+            Worker* wp = W.get();
+            wp->th = std::thread([this, wp] { run(*wp); });
+        }
     }
     ~OpsPipeline() {
         {
@@ -933,28 +967,32 @@ struct OpsPipeline {
             stop = true;
         }
         cv.notify_all();
-        if (th.joinable()) th.join();
+        for (auto& W : workers)
+            if (W->th.joinable()) W->th.join();
         ready.clear();
-        px.release(), py.release(), pds.release();
-        cudaStreamSynchronize(wc.stream);
-        agg.rehome(S->c->stream);
-        S->agg_cache = std::move(agg);
-        cudaStreamDestroy(wc.stream);
+        for (auto& W : workers) {
+            W->px.release(), W->py.release(), W->pds.release();
+            cudaStreamSynchronize(W->wc.stream);
+        }
+        workers[0]->agg.rehome(S->c->stream);
+        S->agg_cache = std::move(workers[0]->agg);
+        for (size_t w = 1; w < workers.size(); ++w) workers[w]->agg = AggCache{};  // freed on its stream
+        for (auto& W : workers) cudaStreamDestroy(W->wc.stream);
     }
 
-    std::unique_ptr<Prepared> produce(int step, double tp) {
+    std::unique_ptr<Prepared> produce(Worker& W, int step, double tp) {
         auto P = std::make_unique<Prepared>();
         const auto t0 = std::chrono::steady_clock::now();
         P->step = step;
         P->t_new = tp + S->dt;
         P->moving = tp < S->geom_static_after;
         if (!P->moving) return P;
-        for (auto& b : bodies) b.move_to(P->t_new);
-        P->bodies = bodies;
-        Ctx* c = &wc;
+        for (auto& b : W.bodies) b.move_to(P->t_new);
+        P->bodies = W.bodies;
+        Ctx* c = &W.wc;
         try {
             std::vector<double> hx, hy, hds;
-            for (const auto& b : bodies)
+            for (const auto& b : W.bodies)
                 for (int p = 0; p < b.n(); ++p) {
                     hx.push_back(b.x[p]);
                     hy.push_back(b.y[p]);
@@ -964,63 +1002,67 @@ struct OpsPipeline {
             const double uni[4] = {g.uniform_region.x0, g.uniform_region.x1, g.uniform_region.y0, g.uniform_region.y1};
             check_support(uni, g.h_min, S->n_b, hx.data(), hy.data());
             const size_t nb = (size_t)std::max(S->n_b, 1);
-            if (px.n != nb) px.alloc(c, nb), py.alloc(c, nb), pds.alloc(c, nb);
-            h2d(c, px.p, hx.data(), hx.size());
-            h2d(c, py.p, hy.data(), hy.size());
-            h2d(c, pds.p, hds.data(), hds.size());
-            assemble_eh_dev(c, *S->gd, S->n_b, px.p, py.p, pds.p, &P->E, nullptr);
+            if (W.px.n != nb) W.px.alloc(c, nb), W.py.alloc(c, nb), W.pds.alloc(c, nb);
+            h2d(c, W.px.p, hx.data(), hx.size());
+            h2d(c, W.py.p, hy.data(), hy.size());
+            h2d(c, W.pds.p, hds.data(), hds.size());
+            assemble_eh_dev(c, *S->gd, S->n_b, W.px.p, W.py.p, W.pds.p, &P->E, nullptr);
             coupled_refresh(c, S->rcache, S->G, P->E, S->BN, &P->Q, &P->QT, &P->lhs2);
             for (Mat* m : {P->Q, P->QT, P->lhs2}) mat_plan(c, m);
             const bool freezing = P->t_new >= S->geom_static_after;
             P->rebuild = S->force_rebuild || freezing || step % S->n_pc == 0;
-            if (P->rebuild) P->hier = sa_build(c, P->lhs2, S->sa, &agg);
+            if (P->rebuild) P->hier = sa_build(c, P->lhs2, S->sa, &W.agg);
             sync(c);
         } catch (const Error& e) {
-            cudaStreamSynchronize(wc.stream);
+            cudaStreamSynchronize(W.wc.stream);
             P->err_code = e.code;
             P->err = e.what();
         } catch (const std::exception& e) {
-            cudaStreamSynchronize(wc.stream);
+            cudaStreamSynchronize(W.wc.stream);
             P->err_code = IBMGPU_ECUDA;
             P->err = e.what();
         }
-        P->launches = wc.launches;
-        wc.launches = 0;
+        P->launches = W.wc.launches;
+        W.wc.launches = 0;
         P->worker_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         return P;
     }
 
-    void run() {
-        cudaSetDevice(wc.device);
+    void run(Worker& W) {
+        cudaSetDevice(W.wc.device);
+        const int cap = depth * (int)workers.size();
         for (;;) {
             int step;
             double tp;
             {
                 std::unique_lock<std::mutex> lk(mu);
-                cv.wait(lk, [&] { return stop || (!finished && (int)ready.size() < depth); });
+                cv.wait(lk, [&] { return stop || (next_step < finish_step && (int)ready.size() + in_flight < cap); });
                 if (stop) return;
-                step = next_step;
+                step = next_step++;
                 tp = t_prev;
+                t_prev = tp + S->dt;  // the same sum the main timeline forms (P->t_new)
+                ++in_flight;
             }
-            auto P = produce(step, tp);
+            auto P = produce(W, step, tp);
             {
                 std::lock_guard<std::mutex> lk(mu);
-                if (!P->moving || P->err_code) finished = true;
-                t_prev = P->t_new;
-                ++next_step;
-                ready.push_back(std::move(P));
+                if (!P->moving || P->err_code) finish_step = std::min(finish_step, step + 1);
+                --in_flight;
+                ready[step] = std::move(P);
             }
             cv.notify_all();
         }
     }
 
-    // the prepared operators of `step` (waits for them); nullptr if the pipeline is on another step
+    // the prepared operators of `step` (waits for them); nullptr if the pipeline cannot produce it
     std::unique_ptr<Prepared> take(int step) {
         std::unique_lock<std::mutex> lk(mu);
-        cv.wait(lk, [&] { return !ready.empty(); });
-        if (ready.front()->step != step) return nullptr;
-        auto P = std::move(ready.front());
-        ready.pop_front();
+        if (step < first_step) return nullptr;
+        cv.wait(lk, [&] { return ready.count(step) || step >= finish_step; });
+        auto it = ready.find(step);
+        if (it == ready.end()) return nullptr;
+        auto P = std::move(it->second);
+        ready.erase(it);
         lk.unlock();
         cv.notify_all();
         return P;
