@@ -115,3 +115,44 @@ def test_ineligible_matrices_keep_explicit_transfers():
     h = ibm.build_sa_hierarchy(A)
     assert h.transfers(1) is False
     assert ibm.sa_apply(h, np.ones(300)).shape == (300,)
+
+
+_C16_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle import oracle as O
+from paper_1109_3524_b200 import ibm
+A = ibm.SparseMatrix.from_host(O.poisson5(320))
+h = ibm.build_sa_hierarchy(A)
+out, kinds = {}, []
+rng = np.random.default_rng(4)
+for l in range(h.n_levels):
+    lv = h.level(l)
+    for k in ("A", "P", "Pt"):
+        m = lv[k]
+        out["%s%d" % (k, l)] = m.spmv(rng.uniform(-1, 1, m.cols()))
+        kinds.append(m.format_bytes()[1])
+np.savez(sys.argv[2], kinds=np.array(kinds), **out)
+"""
+
+
+def test_sixteen_bit_column_codes_are_bitwise(tmp_path):
+    """IBMGPU_C16=1 (off by default since the level-0 transfers): the SELL kernels over 16-bit
+    column codes give the same bits as over int32 columns, on every SA level of a 102k-row
+    Poisson hierarchy."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("0", "1"):
+        f = tmp_path / ("c16_%s.npz" % flag)
+        env = dict(os.environ, IBMGPU_C16=flag)
+        r = subprocess.run([sys.executable, "-c", _C16_SCRIPT, root, str(f)], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[flag] = np.load(f)
+    assert any(k & 16 for k in res["1"]["kinds"]) and not any(k & 16 for k in res["0"]["kinds"])
+    for k in res["0"].files:
+        if k != "kinds":
+            assert np.array_equal(res["0"][k], res["1"][k]), k
