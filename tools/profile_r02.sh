@@ -15,5 +15,5 @@ for w in s4m c2; do
       > $O/ncu_traffic_$w.log 2>&1
 done
 IBMGPU_EAGER=1 ncu --profile-from-start off --set full --import-source on --clock-control none \
-    -k regex:k_spmv_ -s 60 -c 10 -o $O/full_s4m python tools/profile_step.py --workload s4m > $O/ncu_full.log 2>&1
+    -k regex:"k_spmv_|k_xfer_|k_symv" -s 60 -c 16 -o $O/full_s4m python tools/profile_step.py --workload s4m > $O/ncu_full.log 2>&1
 echo done > $O/done
