@@ -173,6 +173,12 @@ def run_ours(args, rank: int, world: int):
         import torch.distributed as dist
         idt = torch.zeros(128, dtype=torch.uint8)
         if rank == 0:
+            # rank 0 logs its communicator init (NCCL_DEBUG=INFO, INIT subsystem) to a file, so the
+            # line can show that the communicator really spans `world` ranks
+            if "NCCL_DEBUG" not in os.environ:
+                os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+                os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT",
+                                  NCCL_DEBUG_FILE=os.path.join(ROOT, "gpurun_out", "nccl_rank0.%p.log"))
             idt = torch.frombuffer(bytearray(ibm.nccl_unique_id()), dtype=torch.uint8).clone()
         dist.broadcast(idt, 0)
         ctx = ibm.Context(local, nranks=world, rank=rank, nccl_id=bytes(idt.numpy().tobytes()))
@@ -281,7 +287,29 @@ def run_ours(args, rank: int, world: int):
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    if slab and rank == 0:
+        out["comm"] = nccl_init_record(world)
     return out, st
+
+
+def nccl_init_record(world: int) -> dict:
+    """Rank 0's NCCL init log (bench.py sets NCCL_DEBUG=INFO/INIT with a per-process file): the
+    communicator size NCCL reported, so the line shows whether it really spans all ranks."""
+    import re
+    path = os.path.join(ROOT, "gpurun_out", "nccl_rank0.%d.log" % os.getpid())
+    rec = {"backend": "nccl", "log": os.path.relpath(path, ROOT), "nranks_logged": None, "nranks_ok": None}
+    try:
+        txt = open(path).read()
+    except OSError:
+        return rec
+    n = [int(m) for m in re.findall(r"ncclCommInitRank comm \S+ rank \d+ nranks (\d+)", txt)]
+    if n:
+        rec["nranks_logged"] = n[-1]
+        rec["nranks_ok"] = n[-1] == world
+    m = re.search(r"NCCL version (\S+)", txt)
+    if m:
+        rec["version"] = m.group(1)
+    return rec
 
 
 def case_probe(args, name: str) -> dict:

@@ -35,9 +35,15 @@ def main():
     ap.add_argument("--min-dist-rows", type=int, default=200000)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--iters", type=int, default=0, help="force exactly this many iterations (timing only)")
+    ap.add_argument("--nccl", action="store_true",
+                    help="one-rank NCCL communicator: the R virtual ranks' halos go through ncclSend/ncclRecv "
+                         "to self and every allreduce through ncclAllReduce (captured in the iteration graph)")
     a = ap.parse_args()
     cfg, h_min, dt, desc = workload(a.workload)
-    st = ibm.Stepper(os.path.join(CASES, cfg + ".cfg"), h_min=h_min, dt=dt)
+    kw = {}
+    if a.nccl:
+        kw["ctx"] = ibm.Context(0, nranks=1, rank=0, nccl_id=ibm.nccl_unique_id())
+    st = ibm.Stepper(os.path.join(CASES, cfg + ".cfg"), h_min=h_min, dt=dt, **kw)
     ctx = st.ctx
     A = st.op("lhs2")
     n = A.rows()
@@ -47,7 +53,7 @@ def main():
     b = A.spmv(w)
     M = ibm.SaPreconditioner(st.hierarchy())
     bd = ibm.DeviceVector.from_host(b, ctx)
-    out = {"workload": a.workload, "desc": desc, "n": n, "results": []}
+    out = {"workload": a.workload, "desc": desc, "n": n, "nccl": a.nccl, "results": []}
 
     def timed(fn):
         fn()
@@ -90,7 +96,7 @@ def main():
 
         ms, r = timed(dist_solve)
         info = ds.info()
-        out["results"].append({"mode": f"loopback R={R}", "ms": round(ms, 3), "iters": r.iterations,
+        out["results"].append({"mode": f"{'nccl-self' if a.nccl else 'loopback'} R={R}", "backend": info["loopback"], "ms": round(ms, 3), "iters": r.iterations,
                                "ms_per_iter": round(ms / r.iterations, 4),
                                "per_rank_ms_per_iter": round(ms / r.iterations / R, 4),
                                "dist_levels": info["dist_levels"], "levels": info["levels"],
