@@ -129,7 +129,7 @@ inline XferPlan xfer_plan(const Hier* h) {
 // amg_setup.cu
 Hier* sa_build(Ctx* c, const Mat* A, const ibm_sa_options& o, AggCache* cache = nullptr);
 int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& agg,
-                     AggCache::Lv* cache = nullptr, bool* hit = nullptr);
+                     AggCache::Lv* cache = nullptr, bool* hit = nullptr, int grid_S = 0);
 // dense.cu
 void dense_spd_inverse(Ctx* c, const Mat* Ac, double* inv);  // factor (dense.hpp:20-40) + inverse
 void launch_dense_gemv(Ctx* c, int n, const double* Ainv, const double* x, double* y, const int* done,

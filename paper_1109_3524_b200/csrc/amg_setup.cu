@@ -383,6 +383,145 @@ inline size_t chunk_smem(int n, int cap) {
     return sizeof(int) * (words + 2 * (kChunk + 4) + kChunk + 8 + 2 * (size_t)cap);
 }
 
+// ---------------------------------------------------------------- pass 1 on a grid-shaped graph
+// When every strength edge of row i goes to i-S, i-1, i+1 or i+S of a grid of NY lines of S
+// cells (the level-0 pressure stencil), the sequential greedy of amg.hpp:84-96 is a recurrence
+// with short reach. In index order, the decision for cell (j, x) needs:
+//   * its own coverage so far: seed(j, x-1) over a +1 edge, or seed(j-1, x) over a +S edge;
+//   * for a -S edge, whether (j-1, x) was covered by a seed before (j, x):
+//     seed(j-1, x) itself, seed(j-1, x-+1) over +-1 edges, or seed(j-2, x) over +S;
+//   * for a -1 edge, whether (j, x-1) was covered: seed(j, x-1), seed(j, x-2) over +1, or
+//     seed(j-1, x-1) over +S;
+//   * for a +1 edge, whether (j, x+1) was covered: only seed(j-1, x+1) over +S can have;
+//   * nothing for a +S edge: no earlier seed reaches (j+1, x).
+// So a line only needs the line above's decisions two columns ahead. A warp runs 32 lines
+// (lane l is line 32w + l, two columns behind lane l - 1), passing each step's two bits down by
+// shuffle. The warp below reads its top line's bits from the warp above through global words
+// published every 32 columns. The output is the same seed set as the sequential loop, by
+// construction (tests compare the aggregates with the reference's).
+constexpr int kGridEP = 16;  // ebits row pitch multiple (uint4 loads)
+
+// edge bits per cell: 1 = -S, 2 = -1, 4 = +1, 8 = +S; *bad if an edge is anything else
+__global__ void k_grid_ebits(int n_core, int S, int pitch, const int* __restrict__ srp, const int* __restrict__ sci,
+                             unsigned char* __restrict__ eb, int* __restrict__ bad) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_core) return;
+    const int x = i % S, j = i / S;
+    unsigned b = 0;
+    for (int k = srp[i]; k < srp[i + 1]; ++k) {
+        const int d = sci[k] - i;
+        if (d == -S) b |= 1u;
+        else if (d == -1 && x > 0) b |= 2u;
+        else if (d == 1 && x < S - 1) b |= 4u;
+        else if (d == S) b |= 8u;
+        else atomicOr(bad, 1);
+    }
+    eb[(size_t)j * pitch + x] = (unsigned char)b;
+}
+
+__device__ __forceinline__ unsigned grid_byte(const uint4& q, int k) {  // byte k (0..15) of q
+    const unsigned w = k < 8 ? (k < 4 ? q.x : q.y) : (k < 12 ? q.z : q.w);
+    return (w >> (8 * (k & 3))) & 0xffu;
+}
+
+__global__ void __launch_bounds__(32) k_greedy_grid(int S, int NY, int pitch, const unsigned char* __restrict__ eb,
+                                                    unsigned* hC, unsigned* hS, int* progress, unsigned* ticket,
+                                                    int* status) {
+    __shared__ int ws;
+    if (threadIdx.x == 0) ws = (int)atomicAdd(ticket, 1u);  // warps start in line order
+    __syncwarp();
+    const int w = ws, lane = threadIdx.x;
+    const int j = w * 32 + lane;
+    const bool line = j < NY;
+    const int nwords = (S + 31) / 32;
+    const unsigned char* row = eb + (size_t)(line ? j : 0) * pitch;
+    unsigned covB = 0, sP1 = 0;   // (j, x-1) covered before (j, x); seed(j, x-1) over a +1 edge
+    unsigned outC = 0, outS = 0;  // published: C(j, x-1) and sPS(j, x) of this lane's last column
+    unsigned sPSup = 0;           // sPS(j-1, x), received the step before
+    unsigned accC = 0, accS = 0;  // lane 31: words being assembled
+    int cwC = -1, cwS = -1, have = 0;         // lane 0: cached words of the warp above
+    unsigned vC = 0, vS = 0;
+    uint4 cur = make_uint4(0, 0, 0, 0), nxt = make_uint4(0, 0, 0, 0);
+    if (line) {
+        cur = *reinterpret_cast<const uint4*>(row);
+        if (kGridEP < pitch) nxt = *reinterpret_cast<const uint4*>(row + kGridEP);
+    }
+    // t = -1: lane 0's column -1 step, which fetches sPS of the line above at column 0
+    const int T = S + 1 + 2 * 31;
+    for (int t = -1; t < T; ++t) {
+        const int x = t - 2 * lane;
+        // from the line above: C(j-1, x) and sPS(j-1, x+1) (its previous step's column x+1)
+        unsigned inC = __shfl_up_sync(kFull, outC, 1), inS = __shfl_up_sync(kFull, outS, 1);
+        if (lane == 0) {
+            inC = inS = 0;
+            if (w > 0 && x >= -1 && x < S) {
+                const int need = min(nwords, (x + 1) / 32 + 1);  // words holding x and x+1
+                if (have < need) {
+                    while ((have = *reinterpret_cast<volatile int*>(progress + w - 1)) < need) __nanosleep(32);
+                    __threadfence();
+                }
+                if (x >= 0) {
+                    if (x / 32 != cwC) cwC = x / 32, vC = __ldcg(hC + (size_t)(w - 1) * nwords + cwC);
+                    inC = (vC >> (x & 31)) & 1u;
+                }
+                if (x + 1 < S) {
+                    if ((x + 1) / 32 != cwS) cwS = (x + 1) / 32, vS = __ldcg(hS + (size_t)(w - 1) * nwords + cwS);
+                    inS = (vS >> ((x + 1) & 31)) & 1u;
+                }
+            }
+        }
+        if (x >= 0 && x <= S) {
+            unsigned e = 0;
+            if (line && x < S) {
+                const int k = x & (kGridEP - 1);
+                e = grid_byte(cur, k);
+                if (k == kGridEP - 1) {  // next 16-column window; prefetch the one after
+                    cur = nxt;
+                    if (x + 1 + kGridEP < pitch) nxt = *reinterpret_cast<const uint4*>(row + x + 1 + kGridEP);
+                }
+            }
+            const unsigned cov = sP1 | sPSup;
+            unsigned seed = 0;
+            if (line && x < S) {
+                bool fr = cov == 0;
+                if (e & 1u) fr = fr && !inC;
+                if (e & 2u) fr = fr && !covB;
+                if (e & 4u) fr = fr && !inS;
+                if (fr) {
+                    seed = 1;
+                    status[(size_t)j * S + x] = SEED;
+                }
+            }
+            outC = covB | (seed & ((e >> 1) & 1u));  // C(j, x-1): a -1 edge of this seed covers it
+            outS = seed & ((e >> 3) & 1u);           // sPS(j, x)
+            covB = cov | seed;
+            sP1 = seed & ((e >> 2) & 1u);
+            if (lane == 31 && line) {
+                // an sPS word is complete one column before the C word of the same index: it is
+                // stored at once, and the C word's progress bump (after the fence) publishes both
+                if (x < S) {
+                    accS |= outS << (x & 31);
+                    if ((x & 31) == 31 || x == S - 1) {
+                        hS[(size_t)w * nwords + x / 32] = accS;
+                        accS = 0;
+                    }
+                }
+                if (x >= 1) {
+                    accC |= outC << ((x - 1) & 31);
+                    if (((x - 1) & 31) == 31 || x - 1 == S - 1) {
+                        const int wd = (x - 1) / 32;
+                        hC[(size_t)w * nwords + wd] = accC;
+                        accC = 0;
+                        __threadfence();
+                        atomicExch(progress + w, wd + 1);
+                    }
+                }
+            }
+        }
+        if (x >= -1) sPSup = inS;  // sPS(j-1, x+1): the next column's sPS(j-1, x)
+    }
+}
+
 __global__ void k_seed_flags(int n, const int* __restrict__ status, int* __restrict__ flag) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) flag[i] = status[i] == SEED;
@@ -763,7 +902,8 @@ __global__ void k_neq(int n, const int* __restrict__ a, const int* __restrict__ 
 }
 
 int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& agg, AggCache::Lv* cache,
-                     bool* hit) {
+                     bool* hit, int grid_S) {
+    if (grid_S == 0 && A->kind == SPMV_STENCIL && A->st_S2 == 0) grid_S = A->st_S1;
     if (hit) *hit = false;
     agg.alloc(c, (size_t)std::max(n_core, 1));
     if (n_core == 0) return 0;
@@ -825,12 +965,38 @@ int aggregate_device(Ctx* c, const Mat* A, double theta, int n_core, DBuf<int>& 
     const bool chunk_ok = cap >= 4096;
     const bool lane = pick != "chunkw";
     const bool use_chunk = pick.rfind("chunk", 0) == 0 ? chunk_ok : pick.empty() ? chunk_ok && n_core <= kChunkMax : false;
+    // grid-shaped strength graph (level 0 of a stencil operator): the line-pipelined replica
+    bool grid_ok = false;
+    int gpitch = 0, gwarps = 0;
+    DBuf<unsigned char> gebits;
+    DBuf<unsigned> ghC, ghS;
+    DBuf<int> gprog;
+    if (!use_chunk && grid_S > 1 && n_core % grid_S == 0 && (pick.empty() || pick == "grid")) {
+        const int NY = n_core / grid_S;
+        gpitch = (grid_S + kGridEP - 1) / kGridEP * kGridEP;
+        gwarps = (NY + 31) / 32;
+        gebits.alloc(c, (size_t)NY * gpitch);
+        DBuf<int> gbad(c, 1);
+        CK(cudaMemsetAsync(gbad.p, 0, sizeof(int), c->stream));
+        k_grid_ebits<<<blocks(n_core), 256, 0, c->stream>>>(n_core, grid_S, gpitch, S.rp.p, S.ci.p, gebits.p, gbad.p);
+        CK_LAUNCH(c);
+        grid_ok = d2h_scalar(c, gbad.p) == 0;
+        if (grid_ok) {
+            const size_t nw = (size_t)gwarps * ((grid_S + 31) / 32);
+            ghC.alloc(c, nw), ghS.alloc(c, nw), gprog.alloc(c, (size_t)gwarps);
+            CK(cudaMemsetAsync(gprog.p, 0, sizeof(int) * (size_t)gwarps, c->stream));
+        }
+    }
     if (use_chunk) {
         const size_t smem = chunk_smem(n_core, cap);
         IBM_SMEM_OPTIN(c, k_greedy_chunk<true>);
         IBM_SMEM_OPTIN(c, k_greedy_chunk<false>);
         auto kern = lane ? k_greedy_chunk<true> : k_greedy_chunk<false>;
         kern<<<1, kChunk, smem, c->stream>>>(n_core, S.rp.p, S.ci.p, status.p, cap);
+        CK_LAUNCH(c);
+    } else if (grid_ok) {
+        k_greedy_grid<<<gwarps, 32, 0, c->stream>>>(grid_S, n_core / grid_S, gpitch, gebits.p, ghC.p, ghS.p,
+                                                     gprog.p, ticket.p, status.p);
         CK_LAUNCH(c);
     } else if (pick == "seq") {
         const size_t smem = sizeof(unsigned) * (size_t)((n_core + 31) / 32) + sizeof(int) * (kGD * kGW + kWin + kGD + 1);
@@ -1080,7 +1246,9 @@ Hier* sa_build(Ctx* c, const Mat* A_fine, const ibm_sa_options& o, AggCache* cac
             bool hit = false;
             int n_agg = 0;
             try {
-                n_agg = aggregate_device(c, A, theta_l, n_core, L->agg, cache ? &cache->lv[lev] : nullptr, &hit);
+                // level 0 of a stencil operator: the copy is not planned yet, the input's plan has the stride
+                const int gS = lev == 0 && A_fine->kind == SPMV_STENCIL && A_fine->st_S2 == 0 ? A_fine->st_S1 : 0;
+                n_agg = aggregate_device(c, A, theta_l, n_core, L->agg, cache ? &cache->lv[lev] : nullptr, &hit, gS);
             } catch (...) {
                 rho_f.wait();
                 throw;
