@@ -461,6 +461,7 @@ __global__ void __launch_bounds__(32) k_greedy_grid(int S, int NY, int pitch, co
                     __threadfence();
                 }
                 if (x >= 0) {
+                    IBM_DCHECK(x / 32 < have);
                     if (x / 32 != cwC) cwC = x / 32, vC = __ldcg(hC + (size_t)(w - 1) * nwords + cwC);
                     inC = (vC >> (x & 31)) & 1u;
                 }
@@ -489,6 +490,7 @@ __global__ void __launch_bounds__(32) k_greedy_grid(int S, int NY, int pitch, co
                 if (e & 4u) fr = fr && !inS;
                 if (fr) {
                     seed = 1;
+                    IBM_DCHECK((size_t)j * S + x < (size_t)NY * S);
                     status[(size_t)j * S + x] = SEED;
                 }
             }

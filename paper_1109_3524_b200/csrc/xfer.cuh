@@ -219,7 +219,10 @@ static __global__ void __launch_bounds__(kBlock) k_xfer_restrict(XferPlan X, int
             for (int k0 = b;;) {
                 double sv[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) sv[q] = mi[q] >= 0 ? ld_weak(s + mi[q]) : 0.0;
+                for (int q = 0; q < 8; ++q) {
+                    IBM_DCHECK(mi[q] < X.n_core);
+                    sv[q] = mi[q] >= 0 ? ld_weak(s + mi[q]) : 0.0;
+                }
 #pragma unroll
                 for (int q = 0; q < 8; ++q)
                     if (mi[q] >= 0) acc = addd(acc, sv[q]);
@@ -284,6 +287,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_xfer_up(XferPlan X, const double*
     for (int k = 0; k < kXK2; ++k) {
         const int f = w + 8 * k, j = j0 - 2 + f;
         a2[k] = (f < kXL2 && col && j >= 0 && j < X.NY) ? __ldg(X.agg + j * X.S + ic) : -1;
+        IBM_DCHECK(a2[k] < X.n_agg);
     }
 #pragma unroll
     for (int k = 0; k < kXK1; ++k) {
@@ -346,6 +350,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_xfer_up(XferPlan X, const double*
                 c = addd(c, mul(__ldg(X.A.ev + q), xc));
             }
         }
+        IBM_DCHECK(r < X.n_core);
         if (m1[k] & kXTailCol) X.xk[r] = x[k];
         sink.row(r, b1[k], addd(x[k], mul(w1[k], subd(b1[k], c))), acc);
     }
