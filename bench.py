@@ -118,7 +118,12 @@ def spmv_bytes(rows, cols, nnz):
 
 
 def hier_bytes(h) -> tuple[float, dict]:
-    """B_it2 of one solve-2 SA-PCG iteration."""
+    """Algorithmic bytes of one solve-2 SA-PCG iteration as the solve applies it.
+    B_it2 counts the reference CSR of every operator the reference V-cycle streams (12 B per
+    entry, both P_l and P_l^T). With the level-0 transfers through the stencil (csrc/xfer.cuh) the
+    solve never streams P_0 / P_0^T: their 24 nnz(P_0) bytes are replaced by the aggregate id per
+    fine row (4 n_0), the member lists (4 n_0 + 4 n_1) and t_a (8 n_1). The reference count stays
+    in info["b_it2_reference"]."""
     nl, _, nc = h.info()
     L0 = h.level(0)["A"] if nl else h.coarse_A()
     n0, nnz0 = L0.rows(), L0.nnz()
@@ -131,7 +136,11 @@ def hier_bytes(h) -> tuple[float, dict]:
         b += 24 * A.nnz() + 24 * P.nnz() + 100 * n_l + 20 * n_next
         levels.append(dict(rows=n_l, nnz_A=A.nnz(), nnz_P=P.nnz()))
     b += 8 * nc * nc + 16 * nc
-    return float(b), dict(levels=levels, n_c=nc)
+    applied = b
+    xfer = bool(nl) and h.transfers()
+    if xfer:
+        applied = b - 24 * levels[0]["nnz_P"] + 8 * n0 + 12 * h.level(0)["P"].cols()
+    return float(applied), dict(levels=levels, n_c=nc, b_it2_reference=float(b), level0_transfers=xfer)
 
 
 def load_traffic(workload: str):
@@ -278,7 +287,10 @@ def run_ours(args, rank: int, world: int):
         "roofline": {"kernel": "solve-2 SA-PCG graph launch (SpMV + V-cycle + fused reductions)",
                      "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "frac_of_8tbs": round(achieved / 8000, 4),
-                     "bytes_per_launch": s2_bytes, "b_it2": b_it2,
+                     "bytes_per_launch": s2_bytes, "b_it2": b_it2, "b_it2_reference": hinfo["b_it2_reference"],
+                     "bytes_definition": ("SURVEY 8(d) B_it2 as applied: level-0 P/P^T applied through the stencil "
+                                          "(not streamed) when level0_transfers"),
+                     "level0_transfers": hinfo["level0_transfers"],
                      "traffic": (round(sum(its2) / K * tr["dram_bytes_per_iteration"]) if tr else None),
                      "traffic_per_iteration": tr["dram_bytes_per_iteration"] if tr else None,
                      "traffic_source": tr["source"] if tr else None},
@@ -346,10 +358,12 @@ def flapping_probe(args) -> dict:
     from paper_1109_3524_b200 import ibm
     cfg, h_min, dt, _ = WORKLOADS["flapping"]
     st = ibm.Stepper(os.path.join(CASES, cfg + ".cfg"), h_min=h_min, dt=dt)
-    for _ in range(3):
+    # steady state: the operator pipeline's workers start cold (empty aggregate caches, first
+    # rebuilds mapping fresh pool memory), so the first steps are not timed
+    for _ in range(8):
         st.advance()
     st.ctx.sync()
-    n = 10
+    n = 20
     t0 = time.perf_counter()
     reps = [st.advance() for _ in range(n)]
     st.ctx.sync()
