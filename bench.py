@@ -360,10 +360,10 @@ def flapping_probe(args) -> dict:
     st = ibm.Stepper(os.path.join(CASES, cfg + ".cfg"), h_min=h_min, dt=dt)
     # steady state: the operator pipeline's workers start cold (empty aggregate caches, first
     # rebuilds mapping fresh pool memory), so the first steps are not timed
-    for _ in range(8):
+    for _ in range(6):
         st.advance()
     st.ctx.sync()
-    n = 20
+    n = 40
     t0 = time.perf_counter()
     reps = [st.advance() for _ in range(n)]
     st.ctx.sync()
