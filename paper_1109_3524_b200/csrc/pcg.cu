@@ -13,6 +13,8 @@
 // recursive residual before preconditioning; pAp <= 0 is breakdown with iterations = it-1;
 // iterations counts the SpMVs after the initial residual.
 #include <map>
+#include <mutex>
+#include <vector>
 #include <memory>
 #include <tuple>
 
@@ -256,6 +258,47 @@ struct BodyDotAfterCoarse {  // no-level hierarchy: r.z after the dense solve
 }  // namespace
 
 // ---------------------------------------------------------------- plan
+// Pinned PcgState slots are recycled instead of freed: cudaFreeHost synchronises the whole device,
+// and a moving body retires one solve-2 plan per step — each retirement stalled the solve stream
+// behind the operator pipeline's kernels. A slot is reused once the event recorded on its plan's
+// last stream at retirement has completed (its final device-to-host copy has landed).
+namespace {
+struct PinSlot {
+    PcgState* p;
+    cudaEvent_t ev;
+};
+std::mutex g_pin_mu;
+std::vector<PinSlot> g_pin_free;
+
+PcgState* pin_acquire() {
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        for (size_t i = 0; i < g_pin_free.size(); ++i) {
+            if (cudaEventQuery(g_pin_free[i].ev) == cudaSuccess) {
+                PinSlot sl = g_pin_free[i];
+                g_pin_free.erase(g_pin_free.begin() + (long)i);
+                cudaEventDestroy(sl.ev);
+                return sl.p;
+            }
+        }
+    }
+    PcgState* p = nullptr;
+    CK(cudaMallocHost(&p, sizeof(PcgState)));
+    return p;
+}
+
+void pin_release(PcgState* p, cudaStream_t last) {
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return;  // leak one slot
+    if (cudaEventRecord(ev, last) != cudaSuccess) {
+        cudaEventDestroy(ev);
+        return;
+    }
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back({p, ev});
+}
+}  // namespace
+
 PcgPlan::PcgPlan(Ctx* c, Mat* A_, int kind_, Hier* h_) : A(A_), kind(kind_), h(h_) {
     require(A->rows == A->cols, "pcg: dimension mismatch");
     if (!A->planned) mat_plan(c, A);
@@ -288,14 +331,15 @@ PcgPlan::PcgPlan(Ctx* c, Mat* A_, int kind_, Hier* h_) : A(A_), kind(kind_), h(h
     partials.alloc(c, (size_t)std::max(g, 1) * 2);
     counter.alloc(c, 1);
     CK(cudaMemsetAsync(counter.p, 0, sizeof(unsigned), c->stream));
-    CK(cudaMallocHost(&host_st, sizeof(PcgState)));
+    host_st = pin_acquire();
+    last_stream = c->stream;
     build_graph(c);
 }
 
 PcgPlan::~PcgPlan() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
-    if (host_st) cudaFreeHost(host_st);
+    if (host_st) pin_release(host_st, last_stream);
 }
 
 void PcgPlan::enqueue_init(Ctx* c, cudaStream_t s) {
@@ -378,6 +422,7 @@ void PcgPlan::build_graph(Ctx* c) {
 }
 
 void PcgPlan::run(Ctx* c, const ibm_solver_params& prm, double* hist_dev) {
+    last_stream = c->stream;
     PcgState& H = *host_st;
     H = PcgState{};
     H.rel_tol = prm.rel_tol;

@@ -22,7 +22,8 @@ struct PcgPlan {
     DBuf<PcgState> st;
     DBuf<double> partials;
     DBuf<unsigned> counter;
-    PcgState* host_st = nullptr;  // pinned
+    PcgState* host_st = nullptr;  // pinned (recycled slot, pcg.cu pin_acquire)
+    cudaStream_t last_stream = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     cudaGraphConditionalHandle cond = 0;

@@ -1200,25 +1200,36 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
     CK(cudaEventRecord(S->ev[1], s));
     nvtxRangePop();
     nvtxRangePushA("solve 1 (pcg-diag)");
-    ibm_solve_result r1;
+    ibm_solve_result r1{};
+    // Single GPU: solve 1's outcome (and the boundary flux check) is read after the step's one
+    // final synchronisation. Solve 2 and the projection are queued behind it right away, and the
+    // host builds solve 2's plan while the GPU runs solve 1; on a failure the step reports
+    // exactly what the in-order checks would and leaves the state untouched (stepper.hpp:266-276).
+    const auto check_solve1 = [&] {
+        if (S->sd_host->bc_err)
+            fail(IBMGPU_ECUDA,
+                 "boundary: prescribed velocities have nonzero net flux and no convective edge to absorb it");
+        rep->solve1_iters = r1.iterations;
+        rep->solve1_res = r1.rel_residual;
+        rep->bc_cfl = S->max_cfl;
+        if (r1.status != 0) {
+            // as in the reference, the boundary state has already advanced (stepper.hpp:271)
+            set_err(rep, "momentum solve did not converge (rel residual " + fmt_res(r1.rel_residual) + ")");
+            return false;
+        }
+        return true;
+    };
     if (distributed) {
         dist_solve(S->dist1, b1, qs, S->p1, &r1, nullptr);
         CK(cudaEventRecord(S->ev[2], s));
+        CK(cudaMemcpyAsync(S->sd_host, S->sd.p, sizeof(StepDev), cudaMemcpyDeviceToHost, s));
+        sync(c);
+        nvtxRangePop();
+        if (!check_solve1()) return;
     } else {
         P1->run(c, S->p1, nullptr);
         CK(cudaEventRecord(S->ev[2], s));
-        P1->finish(c, &r1);
-    }
-    if (d2h_scalar(c, &S->sd.p->bc_err))
-        fail(IBMGPU_ECUDA, "boundary: prescribed velocities have nonzero net flux and no convective edge to absorb it");
-    nvtxRangePop();
-    rep->solve1_iters = r1.iterations;
-    rep->solve1_res = r1.rel_residual;
-    rep->bc_cfl = S->max_cfl;
-    if (r1.status != 0) {
-        // as in the reference, the boundary state has already advanced (stepper.hpp:271)
-        set_err(rep, "momentum solve did not converge (rel residual " + fmt_res(r1.rel_residual) + ")");
-        return;
+        nvtxRangePop();
     }
     // stage 2 (single GPU: one graph launch; distributed: row-slab PCG, dist.cu)
     nvtxRangePushA("solve 2 (rhs2 + pcg-sa)");
@@ -1235,22 +1246,15 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
     launch_spmv(c, S->QT, XPlain{qs}, EpiRhs2{bc2, n_p, 0, S->ub.p, b2}, s);
     d2d(c, lam, S->lambda.p, (size_t)S->n_lambda);
     CK(cudaEventRecord(S->ev[3], s));
-    ibm_solve_result r2;
+    ibm_solve_result r2{};
     if (distributed) {
         dist_solve(S->dist, b2, lam, S->p2, &r2, nullptr);
         CK(cudaEventRecord(S->ev[4], s));
     } else {
         P2->run(c, S->p2, nullptr);
         CK(cudaEventRecord(S->ev[4], s));
-        P2->finish(c, &r2);
     }
     nvtxRangePop();
-    rep->solve2_iters = r2.iterations;
-    rep->solve2_res = r2.rel_residual;
-    if (r2.status != 0) {
-        set_err(rep, "coupled solve did not converge (rel residual " + fmt_res(r2.rel_residual) + ")");
-        return;
-    }
     // stage 3: projection q = q* - B^N (Q lambda)
     NvtxRange proj_range("projection + invariants");
     if (S->bn_diagonal) {
@@ -1265,6 +1269,17 @@ void advance(ibmgpu_stepper* S, ibm_step_report* rep) {
     CK(cudaEventRecord(S->ev[6], s));
     CK(cudaMemcpyAsync(S->sd_host, S->sd.p, sizeof(StepDev), cudaMemcpyDeviceToHost, s));
     sync(c);
+    if (!distributed) {
+        P1->finish(c, &r1);  // already complete: reads the solve's pinned state
+        P2->finish(c, &r2);
+        if (!check_solve1()) return;
+    }
+    rep->solve2_iters = r2.iterations;
+    rep->solve2_res = r2.rel_residual;
+    if (r2.status != 0) {
+        set_err(rep, "coupled solve did not converge (rel residual " + fmt_res(r2.rel_residual) + ")");
+        return;
+    }
     const StepDev& sd = *S->sd_host;
     float ms[6];
     CK(cudaEventElapsedTime(&ms[0], S->ev[0], S->ev[1]));  // explicit
