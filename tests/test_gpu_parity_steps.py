@@ -173,3 +173,24 @@ def test_s4m_three_steps(ref):
     """BASELINE configs[2], the north-star S-4M case as the bench runs it (2040^2, n_lambda 4,167,884,
     dt 1.25e-4 — at dt 2.5e-4 the reference itself blows up from step 4): 3 steps."""
     run_pair(ref, "cylinder_re3000", 3, h_min=0.001, dt=1.25e-4, hier=False)
+
+
+@pytest.mark.parametrize("section,msg", [("solver1", "momentum solve did not converge"),
+                                         ("solver2", "coupled solve did not converge")])
+def test_nonconverged_solve_reports_like_the_reference(ref, tmp_path, section, msg):
+    """stepper.hpp:266-276 / :305-309: a solve that hits max_iters fails the step with the same
+    message, and the flow state is left as it was. On the device both solves are queued before
+    the step's single synchronisation, so this pins that a failed solve 1 still stops the step."""
+    path = case_with(tmp_path, "cylinder_re40_smoke", "[%s]\nmax_iters = 1\nrel_tol = 1e-12" % section)
+    st = ibm.Stepper(path)
+    rc = ref.case(path)
+    for _ in range(3):  # the impulsive start's first momentum solve converges at its initial guess
+        q0, lam0 = st.get("q"), st.get("lambda")
+        r = st.advance()
+        r_ref = rc.step()
+        assert bool(r.ok) == bool(r_ref["ok"]), (r.message, r_ref["message"])
+        if not r.ok:
+            break
+    assert not r.ok and not r_ref["ok"]
+    assert msg in r.message and msg in r_ref["message"], (r.message, r_ref["message"])
+    assert np.array_equal(st.get("q"), q0) and np.array_equal(st.get("lambda"), lam0)
