@@ -927,6 +927,7 @@ struct OpsPipeline {
     double t_prev = 0.0;      // time before next_step
     int in_flight = 0;
     int finish_step = INT_MAX;  // first step that was not moving (or failed): nothing after it
+    int taken_upto = INT_MIN;   // last step handed to the stepper
     bool stop = false;
 
     static int worker_count() {
@@ -1057,12 +1058,14 @@ struct OpsPipeline {
     // the prepared operators of `step` (waits for them); nullptr if the pipeline cannot produce it
     std::unique_ptr<Prepared> take(int step) {
         std::unique_lock<std::mutex> lk(mu);
-        if (step < first_step) return nullptr;
+        // a step before the timeline, or one already taken (a failed step being repeated)
+        if (step < first_step || step <= taken_upto) return nullptr;
         cv.wait(lk, [&] { return ready.count(step) || step >= finish_step; });
         auto it = ready.find(step);
         if (it == ready.end()) return nullptr;
         auto P = std::move(it->second);
         ready.erase(it);
+        taken_upto = step;
         lk.unlock();
         cv.notify_all();
         return P;
