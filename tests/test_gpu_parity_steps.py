@@ -194,3 +194,15 @@ def test_nonconverged_solve_reports_like_the_reference(ref, tmp_path, section, m
     assert not r.ok and not r_ref["ok"]
     assert msg in r.message and msg in r_ref["message"], (r.message, r_ref["message"])
     assert np.array_equal(st.get("q"), q0) and np.array_equal(st.get("lambda"), lam0)
+
+
+@pytest.mark.timeout(300)
+def test_failed_moving_step_can_be_repeated(tmp_path):
+    """A moving-body step that fails (solve 2 at max_iters) consumed its prepared operators; calling
+    advance() again must restart the operator pipeline for that step, not wait for operators that
+    were already handed out (stepper.cu OpsPipeline::take)."""
+    path = case_with(tmp_path, "flapping_smoke", "[solver2]\nmax_iters = 1\nrel_tol = 1e-12")
+    st = ibm.Stepper(path)
+    for _ in range(3):
+        r = st.advance()
+        assert not r.ok and "coupled solve did not converge" in r.message
