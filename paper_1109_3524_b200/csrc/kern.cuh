@@ -699,7 +699,21 @@ inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
     } else if (A->kind == SPMV_SELLW) {
         const int sb = (A->n_short + kBlock - 1) / kBlock;
         grid = sb + (A->n_long + kBlock / 32 - 1) / (kBlock / 32);
-        const bool wide = A->n_short < c->num_sms * 1024 && A->nnz >= 40ll * A->rows;  // few, long rows
+        static const int wide_env = [] {  // IBMGPU_SELLW_WIDE=0/1 forces the 4- / 8-entry stage (A/B)
+            const char* e = std::getenv("IBMGPU_SELLW_WIDE");
+            return e ? std::atoi(e) : -1;
+        }();
+        // the 8-entry stage while the slots are under 2560 per SM: more loads in flight per thread
+        // when the grid is too small to hide latency with warps (C2 L1 320k rows: C2 -2%, S-4M
+        // -0.5%; the 1.2M-row S-4M A_1 stays on 4). IBMGPU_SELLW_WIDE_ROWS (A/B): the threshold;
+        // 1024 restores the old rule (which also asked for >= 40 entries per row)
+        static const int wide_rows = [] {
+            const char* e = std::getenv("IBMGPU_SELLW_WIDE_ROWS");
+            return e ? std::atoi(e) : 2560;
+        }();
+        const bool wide = wide_env >= 0 ? wide_env == 1
+                                        : (long long)A->n_short < (long long)c->num_sms * wide_rows &&
+                                              (wide_rows > 1024 || A->nnz >= 40ll * A->rows);  // few, long rows
         auto go = [&](auto kern, auto cs) {
             launch_k(c, kern, grid, kBlock, s, A->n_short, A->rp.p, A->perm.p, A->sell_off.p, cs, A->sell_v.p, xf,
                      epi, sb, (const int*)A->long_rows.p, A->n_long, (const int*)A->ci.p, (const double*)A->v.p);
