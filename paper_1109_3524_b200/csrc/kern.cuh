@@ -445,17 +445,20 @@ __device__ __forceinline__ double row_sum_inorder(int row, const int* __restrict
 // kU entries per software-pipeline stage. A matrix with few rows (every row a thread, < ~1000
 // threads per SM) cannot hide DRAM latency with more warps, only with more loads in flight per
 // thread: those launch the kU = 8 instance (its registers do not matter at that occupancy).
+#ifndef IBMGPU_SELLW_WIDE_MINB
+#define IBMGPU_SELLW_WIDE_MINB 2
+#endif
 #ifndef IBMGPU_SELLW_MINB
 #define IBMGPU_SELLW_MINB 4
 #endif
 template <class XF, class Epi, int kU = 4, class CS = Cols32>
-__global__ void __launch_bounds__(kBlock, kU == 4 ? IBMGPU_SELLW_MINB : 2) k_spmv_sellw(int rows, const int* __restrict__ rp,
+__global__ void __launch_bounds__(kBlock, kU == 4 ? IBMGPU_SELLW_MINB : IBMGPU_SELLW_WIDE_MINB) k_spmv_sellw(int rows, const int* __restrict__ rp,
                                                           const int* __restrict__ perm, const int* __restrict__ off,
                                                           CS cs, const double* __restrict__ v,
                                                           XF xf, Epi epi, int sblocks, const int* __restrict__ long_rows,
                                                           int n_long, const int* __restrict__ csr_ci,
                                                           const double* __restrict__ csr_v) {
-    pdl_release_early(kU == 4 ? IBMGPU_SELLW_MINB : 2);
+    pdl_release_early(kU == 4 ? IBMGPU_SELLW_MINB : IBMGPU_SELLW_WIDE_MINB);
     constexpr int NR = Epi::NR;
     constexpr int U = kU;
     double acc[NR > 0 ? NR : 1];
@@ -473,7 +476,7 @@ __global__ void __launch_bounds__(kBlock, kU == 4 ? IBMGPU_SELLW_MINB : 2) k_spm
             if (lane == 0) epi.row(row, s, acc);
         }
         if (skip) return;
-        pdl_release_late(kU == 4 ? IBMGPU_SELLW_MINB : 2);
+        pdl_release_late(kU == 4 ? IBMGPU_SELLW_MINB : IBMGPU_SELLW_WIDE_MINB);
         if constexpr (NR > 0) block_partial<NR>(acc, epi.slot());
         return;
     }
@@ -520,7 +523,7 @@ __global__ void __launch_bounds__(kBlock, kU == 4 ? IBMGPU_SELLW_MINB : 2) k_spm
     }
     if (skip) return;
     if (row >= 0) epi.row(row, s, acc);
-    pdl_release_late(kU == 4 ? IBMGPU_SELLW_MINB : 2);
+    pdl_release_late(kU == 4 ? IBMGPU_SELLW_MINB : IBMGPU_SELLW_WIDE_MINB);
     if constexpr (NR > 0) {
         block_partial<NR>(acc, epi.slot());
     }
