@@ -757,30 +757,57 @@ struct DenseChunk {
     double a[kDenseChunk];
 };
 
+// Wider outputs (up to kDenseWideMax columns): `win` gives each row a window [base, base + ncols)
+// holding all its columns (the rows of P^T A on coarse levels are spatially local). A row whose
+// span exceeds the window uses this CTA's full-width accumulator and bitmap in global memory
+// (gacc / gbits, zero between rows like the shared ones) — same order of additions either way.
+struct DenseWide {
+    const int* lo;   // per row: first column (window base); nullptr: no windows
+    const int* hi;   // per row: last column
+    int full;        // output width
+    double* gacc;    // per CTA: full doubles (numeric)
+    unsigned* gbits; // per CTA: (full + 31) / 32 words
+};
+
 template <bool kNumeric>
 __global__ void __launch_bounds__(kDenseThreads) k_dense_rows(int r0, int rows, int ncols, const int* __restrict__ arp,
                                                              const int* __restrict__ aci, const double* __restrict__ av,
                                                              const int* __restrict__ brp, const int* __restrict__ bci,
                                                              const double* __restrict__ bv, int* __restrict__ cnt,
                                                              const int* __restrict__ crp, int* __restrict__ cci,
-                                                             double* __restrict__ cv, unsigned* __restrict__ next) {
+                                                             double* __restrict__ cv, unsigned* __restrict__ next,
+                                                             DenseWide win) {
     extern __shared__ double dsm[];
-    double* acc = dsm;  // ncols (numeric only)
-    unsigned* bits = reinterpret_cast<unsigned*>(kNumeric ? dsm + ncols : dsm);
-    const int nwords = (ncols + 31) >> 5;
+    double* const sacc = dsm;  // ncols (numeric only)
+    unsigned* const sbits = reinterpret_cast<unsigned*>(kNumeric ? dsm + ncols : dsm);
     __shared__ DenseChunk ch;
     __shared__ int s_row, s_total, s_scan[kDenseThreads + 1];
     __shared__ double s_prod[kDenseThreads / 32][32];
     const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-    for (int k = t; k < nwords; k += kDenseThreads) bits[k] = 0u;
+    for (int k = t; k < ((ncols + 31) >> 5); k += kDenseThreads) sbits[k] = 0u;
     if (kNumeric)
-        for (int k = t; k < ncols; k += kDenseThreads) acc[k] = 0.0;
+        for (int k = t; k < ncols; k += kDenseThreads) sacc[k] = 0.0;
     __syncthreads();
     for (;;) {
         if (t == 0) s_row = (int)atomicAdd(next, 1u);
         __syncthreads();
         const int row = s_row;
         if (row >= rows) break;
+        // this row's accumulator: the shared window, or the CTA's full-width global one
+        int base = 0, width = ncols;
+        double* acc = sacc;
+        unsigned* bits = sbits;
+        if (win.lo) {
+            const int lo = win.lo[row], hi = win.hi[row];
+            if (hi - lo < ncols) {
+                base = lo;
+            } else {
+                width = win.full;
+                bits = win.gbits + (size_t)blockIdx.x * ((win.full + 31) >> 5);
+                if (kNumeric) acc = win.gacc + (size_t)blockIdx.x * win.full;
+            }
+        }
+        const int nwords = (width + 31) >> 5;
         const int i = r0 + row, b = arp[i], e = arp[i + 1];
         for (int c0 = b; c0 < e; c0 += kDenseChunk) {
             // chunk of A entries: B-row starts, lengths -> inclusive offsets (block scan)
@@ -822,7 +849,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_rows(int r0, int rows, 
                             hi = mid - 1;
                     }
                     const int jj = ch.bs[lo] + (q - ch.off[lo]);
-                    col = bci[jj];
+                    col = bci[jj] - base;
                     if (kNumeric) p = mul(ch.a[lo], bv[jj]);
                 }
                 if (!kNumeric) {
@@ -870,7 +897,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_rows(int r0, int rows, 
                 while (m) {
                     const int col = (k << 5) + __ffs(m) - 1;
                     m &= m - 1;
-                    cci[o] = col;
+                    cci[o] = col + base;
                     cv[o] = acc[col];
                     acc[col] = 0.0;
                     ++o;
@@ -882,10 +909,45 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_rows(int r0, int rows, 
     }
 }
 
+// first and last output column of each row: the first / last column of the B rows its A entries
+// select (B rows are sorted)
+__global__ void k_row_span(int r0, int rows, const int* __restrict__ arp, const int* __restrict__ aci,
+                           const int* __restrict__ brp, const int* __restrict__ bci, int* __restrict__ lo,
+                           int* __restrict__ hi, int width, unsigned* __restrict__ nwide) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    int a = INT_MAX, z = -1;
+    for (int k = arp[r0 + r]; k < arp[r0 + r + 1]; ++k) {
+        const int j = aci[k], s0 = brp[j], s1 = brp[j + 1];
+        if (s1 > s0) a = min(a, bci[s0]), z = max(z, bci[s1 - 1]);
+    }
+    if (z < 0) a = z = 0;
+    lo[r] = a;
+    hi[r] = z;
+    if (z - a >= width) atomicAdd(nwide, 1u);
+}
+
+constexpr int kDenseWideMax = 131072;  // widest output the windowed path takes (1 MB per CTA scratch)
+
 // spmm_rows by the dense-accumulator kernels; nullptr when the output is too wide
 Mat* spmm_dense(Ctx* c, const Mat* A, int r0, int r1, const Mat* B) {
-    const int rows = r1 - r0, ncols = B->cols;
-    if (rows <= 0 || ncols > kDenseCols || ncols <= 0) return nullptr;
+    const int rows = r1 - r0, full = B->cols;
+    if (rows <= 0 || full > kDenseWideMax || full <= 0) return nullptr;
+    const bool windowed = full > kDenseCols;
+    const int ncols = windowed ? kDenseCols : full;  // shared accumulator width
+    DenseWide win{nullptr, nullptr, full, nullptr, nullptr};
+    DBuf<int> lo, hi;
+    if (windowed) {
+        lo.alloc(c, (size_t)rows), hi.alloc(c, (size_t)rows);
+        DBuf<unsigned> nwide(c, 1);
+        CK(cudaMemsetAsync(nwide.p, 0, sizeof(unsigned), c->stream));
+        k_row_span<<<(rows + 255) / 256, 256, 0, c->stream>>>(r0, rows, A->rp.p, A->ci.p, B->rp.p, B->ci.p, lo.p, hi.p,
+                                                              ncols, nwide.p);
+        CK_LAUNCH(c);
+        // rows that overflow the window run at global-memory speed: worth it while they are few
+        if ((long long)d2h_scalar(c, nwide.p) * 8 > rows) return nullptr;
+        win.lo = lo.p, win.hi = hi.p;
+    }
     const int nwords = (ncols + 31) / 32;
     const size_t sym_smem = sizeof(unsigned) * (size_t)nwords;
     const size_t num_smem = sizeof(double) * (size_t)ncols + sizeof(unsigned) * (size_t)nwords;
@@ -899,18 +961,28 @@ Mat* spmm_dense(Ctx* c, const Mat* A, int r0, int r1, const Mat* B) {
     DBuf<unsigned> next(c, 2);
     CK(cudaMemsetAsync(next.p, 0, 2 * sizeof(unsigned), c->stream));
     DBuf<int> cnt(c, (size_t)rows + 1);
+    DBuf<double> gacc;
+    DBuf<unsigned> gbits;
+    if (windowed) {  // per-CTA full-width scratch for the rows wider than the window (zeroed once)
+        const size_t fw = (size_t)(full + 31) / 32;
+        gbits.alloc(c, fw * (size_t)std::max(gs, gn));
+        CK(cudaMemsetAsync(gbits.p, 0, sizeof(unsigned) * gbits.n, c->stream));
+        gacc.alloc(c, (size_t)full * gn);
+        CK(cudaMemsetAsync(gacc.p, 0, sizeof(double) * gacc.n, c->stream));
+        win.gacc = gacc.p, win.gbits = gbits.p;
+    }
     k_dense_rows<false><<<gs, kDenseThreads, sym_smem, c->stream>>>(r0, rows, ncols, A->rp.p, A->ci.p, A->v.p, B->rp.p,
                                                                      B->ci.p, B->v.p, cnt.p, nullptr, nullptr, nullptr,
-                                                                     next.p);
+                                                                     next.p, win);
     CK_LAUNCH(c);
-    Mat* m = mat_new(c, rows, ncols, 0);
+    Mat* m = mat_new(c, rows, full, 0);
     exclusive_scan_total(c, cnt.p, m->rp.p, rows);
     m->nnz = d2h_scalar(c, m->rp.p + rows);
     m->ci.alloc(c, (size_t)std::max(m->nnz, 1));
     m->v.alloc(c, (size_t)std::max(m->nnz, 1));
     k_dense_rows<true><<<gn, kDenseThreads, num_smem, c->stream>>>(r0, rows, ncols, A->rp.p, A->ci.p, A->v.p, B->rp.p,
                                                                     B->ci.p, B->v.p, nullptr, m->rp.p, m->ci.p, m->v.p,
-                                                                    next.p + 1);
+                                                                    next.p + 1, win);
     CK_LAUNCH(c);
     return m;
 }
@@ -1048,7 +1120,10 @@ Mat* spmm_rows(Ctx* c, const Mat* A, int r0, int r1, const Mat* B) {
             const char* e = std::getenv("IBMGPU_DENSE_SPGEMM");  // IBMGPU_DENSE_SPGEMM=0: hash only
             return !(e && e[0] == '0');
         }();
-        if (dense_on && B->cols <= kDenseCols && total >= 256ll * (r1 - r0))
+        // (windowed, wider outputs: only for rows of >= 1024 products — the level-2 P^T A of a
+        // moving body; at ~300 products per row a CTA per row loses to the hash warps)
+        if (dense_on && total >= 256ll * (r1 - r0) &&
+            (B->cols <= kDenseCols || (B->cols <= kDenseWideMax && total >= 1024ll * (r1 - r0))))
             if (Mat* d = spmm_dense(c, A, r0, r1, B)) return finish_plan(c, d);
         if (total >= 32ll * (r1 - r0))
             if (Mat* h = spmm_hash(c, A, r0, r1, B, rprod.p)) return finish_plan(c, h);
