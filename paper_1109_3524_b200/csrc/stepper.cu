@@ -885,7 +885,7 @@ namespace ibmgpu {
 // the main stream runs the current step's solves. Inputs: the prescribed body positions at each
 // step's t_new (the same sequence of t + dt additions as the stepper), G, B^N and the refresh
 // cache — all constant — so every prepared operator is bit-identical to the in-line one; the
-// main thread only installs them. The worker runs at most `depth` steps ahead.
+// main thread only installs them. The workers run a bounded number of steps ahead (OpsPipeline::run).
 struct Prepared {
     int step = -1;
     double t_new = 0.0;
@@ -921,7 +921,6 @@ struct OpsPipeline {
     std::mutex mu;
     std::condition_variable cv;
     std::map<int, std::unique_ptr<Prepared>> ready;
-    int depth = 2;            // prepared steps ahead per worker
     int first_step = 0;
     int next_step = 0;        // next step to claim
     double t_prev = 0.0;      // time before next_step
@@ -1031,7 +1030,14 @@ struct OpsPipeline {
 
     void run(Worker& W) {
         cudaSetDevice(W.wc.device);
-        const int cap = depth * (int)workers.size();
+        // prepared-but-not-installed steps are bounded (each holds a lhs2 and maybe a hierarchy):
+        // one in flight per worker plus IBMGPU_PIPE_AHEAD ready ahead. Default 3 (flapping, three
+        // workers: 99.6-100 steps/s; 1 ahead: 97.4); large moving cases can lower it for memory
+        static const int ahead = [] {
+            const char* e = std::getenv("IBMGPU_PIPE_AHEAD");
+            return e ? std::max(0, std::atoi(e)) : 3;
+        }();
+        const int cap = (int)workers.size() + ahead;
         for (;;) {
             int step;
             double tp;
