@@ -271,7 +271,7 @@ inline void vcycle_launch(Ctx* c, Hier* h, const double* r_in, double* z_out, co
         const double* b = l == 0 ? r_in : lv.b.p;
         if (l == 0 && h->x0.on) {  // stencil transfers (xfer.cuh): s into lv.r, then b_1 = P^T r1
             const XferPlan X = xfer_plan(h);
-            launch_k(c, k_xfer_down, h->x0.tail_ctas + h->x0.tiles, kBlock, s, X, b, lv.r.p, h->x0.r1t.p, done);
+            launch_k(c, k_xfer_down, h->x0.tail_ctas + h->x0.tiles, kXThreads, s, X, b, lv.r.p, h->x0.r1t.p, done);
             const int n1 = l + 1 < L ? h->levels[1]->A->rows : h->n_dense;
             const int g = (n1 + kBlock - 1) / kBlock;
             if (l + 1 < L) {
@@ -332,7 +332,7 @@ struct LastPlain {
     }
     void xfer(Hier* h, const double* b, const double* e, double* z) const {
         const XSinkPlain sink{z, done};
-        launch_k(c, k_xfer_up<XSinkPlain>, h->x0.tiles, kBlock, s, xfer_plan(h), b, e, sink);
+        launch_k(c, k_xfer_up<XSinkPlain>, h->x0.tiles, kXThreads, s, xfer_plan(h), b, e, sink);
         if (h->x0.tail_ctas)
             launch_k(c, k_xfer_up_tail<XSinkPlain>, h->x0.tail_ctas, kBlock, s, xfer_plan(h), b, e, sink, h->x0.tiles);
     }

@@ -234,7 +234,7 @@ struct LastDot {
     void xfer(Hier* h, const double* b, const double* e, double* z) const {
         const XSinkDot<Fin> sink{z, done, rs, f};
         const XferPlan X = xfer_plan(h);
-        launch_k(c, k_xfer_up<XSinkDot<Fin>>, h->x0.tiles, kBlock, s, X, b, e, sink);
+        launch_k(c, k_xfer_up<XSinkDot<Fin>>, h->x0.tiles, kXThreads, s, X, b, e, sink);
         if (h->x0.tail_ctas)
             launch_k(c, k_xfer_up_tail<XSinkDot<Fin>>, h->x0.tail_ctas, kBlock, s, X, b, e, sink, h->x0.tiles);
         launch_k(c, k_finalize<XSinkDot<Fin>>, 1, kFinThreads, s, sink, h->x0.tiles + h->x0.tail_ctas);

@@ -36,14 +36,25 @@
 namespace ibmgpu {
 
 constexpr int kXOut = 28;        // output columns per tile (lanes 2..29)
-constexpr int kXTJ = 22;         // output lines per tile
+#ifndef IBMGPU_XFER_TJ
+#define IBMGPU_XFER_TJ 22
+#endif
+constexpr int kXTJ = IBMGPU_XFER_TJ;  // output lines per tile
 constexpr int kXL1 = kXTJ + 2;   // band lines (tile + 1): 4 per warp
 constexpr int kXL2 = kXTJ + 4;   // x / y frame lines (tile + 2)
-constexpr int kXK1 = kXL1 / 8;   // band lines per warp
-constexpr int kXK2 = (kXL2 + 7) / 8;
+#ifndef IBMGPU_XFER_WARPS
+#define IBMGPU_XFER_WARPS 8
+#endif
+#ifndef IBMGPU_XFER_MINB
+#define IBMGPU_XFER_MINB 3
+#endif
+constexpr int kXWarps = IBMGPU_XFER_WARPS;  // warps per tile CTA
+constexpr int kXThreads = 32 * kXWarps;
+constexpr int kXK1 = kXL1 / kXWarps;  // band lines per warp
+constexpr int kXK2 = (kXL2 + kXWarps - 1) / kXWarps;
 constexpr int kXTailRows = 8;    // tail rows per CTA (one warp each)
 constexpr unsigned kXTailCol = 128u;  // stencil mask bit 7 (hierarchy copy of A_0): a tail row's column
-static_assert(kXL1 % 8 == 0, "band lines per warp");
+static_assert(kXL1 % kXWarps == 0, "band lines per warp");
 
 struct XferPlan {
     StencilPlan A;  // level-0 band planes + extras (n rows)
@@ -94,13 +105,14 @@ __device__ __forceinline__ double shup(double v) { return __shfl_up_sync(kFull, 
 __device__ __forceinline__ double shdn(double v) { return __shfl_down_sync(kFull, v, 1); }  // lane + 1
 
 // K_D: s = r1 - A^T(wd r1) on core rows, r1 = b - A (wd b); r1 of the tail rows into r1t.
-static __global__ void __launch_bounds__(kBlock, 3) k_xfer_down(XferPlan X, const double* b, double* s_out,
+static __global__ void __launch_bounds__(kXThreads, IBMGPU_XFER_MINB) k_xfer_down(XferPlan X, const double* b, double* s_out,
                                                                 double* r1t, const int* done) {
     __shared__ double sx[kXL2][32];  // x = wd b, frame lines j0-2 ..
     __shared__ double sq4[kXL1][32];  // A_{m,+S} u_m (read by the line below)
     __shared__ double sq0[kXL1][32];  // A_{m,-S} u_m (read by the line above)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (blockIdx.x < X.tail_ctas) {  // tail rows, one warp each
+        if (w >= kXTailRows) return;
         const int t = blockIdx.x * kXTailRows + w;
         pdl_wait();
         if (done && flag_set(done)) return;
@@ -119,7 +131,7 @@ static __global__ void __launch_bounds__(kBlock, 3) k_xfer_down(XferPlan X, cons
     unsigned m1[kXK1];
 #pragma unroll
     for (int k = 0; k < kXK1; ++k) {
-        const int j = j0 - 1 + w + 8 * k;
+        const int j = j0 - 1 + w + kXWarps * k;
         r1c[k] = (col && j >= 0 && j < X.NY) ? j * X.S + ic : -1;
 #pragma unroll
         for (int q = 0; q < 5; ++q) p[k][q] = r1c[k] >= 0 ? __ldg(X.A.v + (size_t)q * X.n + r1c[k]) : 0.0;
@@ -128,7 +140,7 @@ static __global__ void __launch_bounds__(kBlock, 3) k_xfer_down(XferPlan X, cons
     }
 #pragma unroll
     for (int k = 0; k < kXK2; ++k) {
-        const int f = w + 8 * k, j = j0 - 2 + f;
+        const int f = w + kXWarps * k, j = j0 - 2 + f;
         r2c[k] = (f < kXL2 && col && j >= 0 && j < X.NY) ? j * X.S + ic : -1;
         w2[k] = r2c[k] >= 0 ? __ldg(X.wd + r2c[k]) : 0.0;
     }
@@ -141,13 +153,13 @@ static __global__ void __launch_bounds__(kBlock, 3) k_xfer_down(XferPlan X, cons
     if (done && flag_set(done)) return;
 #pragma unroll
     for (int k = 0; k < kXK2; ++k)
-        if (w + 8 * k < kXL2) sx[w + 8 * k][lane] = mul(w2[k], b2[k]);
+        if (w + kXWarps * k < kXL2) sx[w + kXWarps * k][lane] = mul(w2[k], b2[k]);
     __syncthreads();
     // r1 = b - A x on the band lines (column order -S, -1, 0, +1, +S, then tail-column extras)
     double r1[kXK1], c1[kXK1], c2[kXK1], c3[kXK1];
 #pragma unroll
     for (int k = 0; k < kXK1; ++k) {
-        const int f = w + 8 * k;  // band line f = frame line f + 1
+        const int f = w + kXWarps * k;  // band line f = frame line f + 1
         const double xm = sx[f + 1][lane];
         const double xl = shup(xm), xr = shdn(xm);
         double a = 0.0;
@@ -175,7 +187,7 @@ static __global__ void __launch_bounds__(kBlock, 3) k_xfer_down(XferPlan X, cons
     // s_m = r1_m - [A_{m-S,m} u + A_{m-1,m} u + A_mm u + A_{m+1,m} u + A_{m+S,m} u]
 #pragma unroll
     for (int k = 0; k < kXK1; ++k) {
-        const int f = w + 8 * k;
+        const int f = w + kXWarps * k;
         const double cl = shup(c3[k]), cr = shdn(c1[k]);
         if (f >= 1 && f <= kXTJ && r1c[k] >= 0 && lane >= 2 && lane < 2 + kXOut) {
             double c = 0.0;
@@ -269,7 +281,7 @@ struct XSinkDot {
 
 // K_U: z = x + wd (b - A x), x = wd b + P e, with P e applied through the stencil (see top).
 template <class Sink>
-__global__ void __launch_bounds__(kBlock, 3) k_xfer_up(XferPlan X, const double* b, const double* e, Sink sink) {
+__global__ void __launch_bounds__(kXThreads, IBMGPU_XFER_MINB) k_xfer_up(XferPlan X, const double* b, const double* e, Sink sink) {
     __shared__ double sy[kXL2][32];  // y = T e, frame lines j0-2 ..
     __shared__ double sx[kXL1][32];  // x, band lines j0-1 ..
     constexpr int NR = Sink::NR;
@@ -285,13 +297,13 @@ __global__ void __launch_bounds__(kBlock, 3) k_xfer_up(XferPlan X, const double*
     unsigned m1[kXK1];
 #pragma unroll
     for (int k = 0; k < kXK2; ++k) {
-        const int f = w + 8 * k, j = j0 - 2 + f;
+        const int f = w + kXWarps * k, j = j0 - 2 + f;
         a2[k] = (f < kXL2 && col && j >= 0 && j < X.NY) ? __ldg(X.agg + j * X.S + ic) : -1;
         IBM_DCHECK(a2[k] < X.n_agg);
     }
 #pragma unroll
     for (int k = 0; k < kXK1; ++k) {
-        const int j = j0 - 1 + w + 8 * k;
+        const int j = j0 - 1 + w + kXWarps * k;
         r1c[k] = (col && j >= 0 && j < X.NY) ? j * X.S + ic : -1;
 #pragma unroll
         for (int q = 0; q < 5; ++q) p[k][q] = r1c[k] >= 0 ? __ldg(X.A.v + (size_t)q * X.n + r1c[k]) : 0.0;
@@ -309,13 +321,13 @@ __global__ void __launch_bounds__(kBlock, 3) k_xfer_up(XferPlan X, const double*
     const bool skip = sink.skip();
 #pragma unroll
     for (int k = 0; k < kXK2; ++k)
-        if (w + 8 * k < kXL2) sy[w + 8 * k][lane] = mul(t2[k], e2[k]);
+        if (w + kXWarps * k < kXL2) sy[w + kXWarps * k][lane] = mul(t2[k], e2[k]);
     __syncthreads();
     // x = wd b + (y - wd (A y)) on the band lines (core extras are tail columns: y = 0 there)
     double x[kXK1];
 #pragma unroll
     for (int k = 0; k < kXK1; ++k) {
-        const int f = w + 8 * k;
+        const int f = w + kXWarps * k;
         const double ym = sy[f + 1][lane];
         const double yl = shup(ym), yr = shdn(ym);
         double a = 0.0;
@@ -331,7 +343,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_xfer_up(XferPlan X, const double*
     // z = x + wd (b - A x) on the tile
 #pragma unroll
     for (int k = 0; k < kXK1; ++k) {
-        const int f = w + 8 * k;
+        const int f = w + kXWarps * k;
         const double xl = shup(x[k]), xr = shdn(x[k]);
         const int r = r1c[k];
         if (skip || f < 1 || f > kXTJ || r < 0 || lane < 2 || lane >= 2 + kXOut) continue;
