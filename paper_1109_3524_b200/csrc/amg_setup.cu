@@ -1199,6 +1199,7 @@ struct AuxStream {
     }
     ~AuxStream() {
         cudaStreamSynchronize(c.stream);
+        zero_scratch_free(&c);
         cudaEventDestroy(fork);
         cudaEventDestroy(join);
         cudaStreamDestroy(c.stream);

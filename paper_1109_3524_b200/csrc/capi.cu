@@ -109,6 +109,7 @@ int ibmgpu_destroy(ibmgpu_ctx_t c) {
     if (!c) return 0;
     cudaStreamSynchronize(c->stream);
     pcg_cache_free(c);
+    zero_scratch_free(c);
     ctx_free_extras(c);
     nccl_comm_free(c);
     cudaEventDestroy(c->t0);

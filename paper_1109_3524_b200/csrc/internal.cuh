@@ -59,6 +59,10 @@ struct ibmgpu_ctx {
     int eager = 0;              // IBMGPU_EAGER=1: host-looped solves (profiling only)
     int pdl_fence = 0;          // set by plain launches: the next launch_k skips PDL (CK_LAUNCH)
     cudaMemPool_t pool = nullptr;  // the context's own stream-ordered pool (capi.cu ibmgpu_init)
+    // zero-filled scratch kept across calls (sparse_ops.cu windowed dense SpGEMM: its kernels leave
+    // it zero again), so no call allocates and clears hundreds of MB; freed with the context
+    void* zscratch = nullptr;
+    size_t zscratch_bytes = 0;
 };
 
 namespace ibmgpu {
@@ -118,6 +122,24 @@ inline void d2d(Ctx* c, T* dst, const T* src, size_t n) {
     if (n) CK(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyDeviceToDevice, c->stream));
 }
 inline void sync(Ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
+
+// The context's zero-filled scratch, grown (and cleared once) when a call needs more.
+inline void* zero_scratch(Ctx* c, size_t bytes) {
+    if (bytes > c->zscratch_bytes) {
+        if (c->zscratch) CK(cudaFreeAsync(c->zscratch, c->stream));
+        c->zscratch = nullptr;
+        c->zscratch_bytes = 0;
+        CK(cudaMallocFromPoolAsync(&c->zscratch, bytes, c->pool, c->stream));
+        CK(cudaMemsetAsync(c->zscratch, 0, bytes, c->stream));
+        c->zscratch_bytes = bytes;
+    }
+    return c->zscratch;
+}
+inline void zero_scratch_free(Ctx* c) {
+    if (c->zscratch) cudaFreeAsync(c->zscratch, c->stream);
+    c->zscratch = nullptr;
+    c->zscratch_bytes = 0;
+}
 
 // A kernel's dynamic shared-memory limit, raised once to the device's opt-in maximum (minus its
 // static shared memory). Setting it per launch to that launch's size races when two host threads

@@ -961,15 +961,13 @@ Mat* spmm_dense(Ctx* c, const Mat* A, int r0, int r1, const Mat* B) {
     DBuf<unsigned> next(c, 2);
     CK(cudaMemsetAsync(next.p, 0, 2 * sizeof(unsigned), c->stream));
     DBuf<int> cnt(c, (size_t)rows + 1);
-    DBuf<double> gacc;
-    DBuf<unsigned> gbits;
-    if (windowed) {  // per-CTA full-width scratch for the rows wider than the window (zeroed once)
+    if (windowed) {  // per-CTA full-width accumulators for the rows wider than the window: the
+                     // context's zero scratch (the kernels clear what they touch)
         const size_t fw = (size_t)(full + 31) / 32;
-        gbits.alloc(c, fw * (size_t)std::max(gs, gn));
-        CK(cudaMemsetAsync(gbits.p, 0, sizeof(unsigned) * gbits.n, c->stream));
-        gacc.alloc(c, (size_t)full * gn);
-        CK(cudaMemsetAsync(gacc.p, 0, sizeof(double) * gacc.n, c->stream));
-        win.gacc = gacc.p, win.gbits = gbits.p;
+        const size_t acc_b = sizeof(double) * (size_t)full * gn;
+        char* z = static_cast<char*>(zero_scratch(c, acc_b + sizeof(unsigned) * fw * (size_t)std::max(gs, gn)));
+        win.gacc = reinterpret_cast<double*>(z);
+        win.gbits = reinterpret_cast<unsigned*>(z + acc_b);
     }
     k_dense_rows<false><<<gs, kDenseThreads, sym_smem, c->stream>>>(r0, rows, ncols, A->rp.p, A->ci.p, A->v.p, B->rp.p,
                                                                      B->ci.p, B->v.p, cnt.p, nullptr, nullptr, nullptr,

@@ -972,6 +972,7 @@ struct OpsPipeline {
         ready.clear();
         for (auto& W : workers) {
             W->px.release(), W->py.release(), W->pds.release();
+            zero_scratch_free(&W->wc);
             cudaStreamSynchronize(W->wc.stream);
         }
         workers[0]->agg.rehome(S->c->stream);
