@@ -681,6 +681,64 @@ __global__ void __launch_bounds__(kBlock, IBMGPU_ADAPT_MINB) k_spmv_adapt(AdaptP
 }
 
 // Launch helper: dispatch on the matrix's plan.
+// Warp per row with a tree reduction, for the long-row coarse levels (replaces k_spmv_adapt where
+// the mean row has >= 48 entries): lanes stride the row four entries at a time with every load of
+// a batch issued first (the last, partial batch too), then five shuffle steps. Deterministic (fixed order), not bitwise with spmv_into — the
+// same contract as the adaptive kernel. Warps take rows gw, gw + warps, ...
+template <class XF, class Epi>
+__global__ void __launch_bounds__(kBlock, 8) k_spmv_warprow(int rows, const int* __restrict__ rp,
+                                                             const int* __restrict__ ci, const double* __restrict__ v,
+                                                             XF xf, Epi epi) {
+    pdl_release_early(8);
+    constexpr int NR = Epi::NR;
+    double acc[NR > 0 ? NR : 1];
+#pragma unroll
+    for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
+    const int lane = threadIdx.x & 31;
+    const int nw = gridDim.x * (kBlock / 32);
+    int i = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+    int b = i < rows ? __ldg(rp + i) : 0, e = i < rows ? __ldg(rp + i + 1) : 0;
+    pdl_wait();
+    const bool skip = epi.skip();
+    for (; i < rows; i += nw) {
+        double s = 0.0;
+        int k = b + lane;
+        for (; k + 96 < e; k += 128) {
+            int c[4];
+            double a[4], x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c[u] = __ldg(ci + k + 32 * u), a[u] = __ldg(v + k + 32 * u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = xf(c[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s = addd(s, mul(a[u], x[u]));
+        }
+        if (k < e) {  // the last (partial) batch: all its loads issued at once
+            int c[4];
+            double a[4], x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool in = k + 32 * u < e;
+                c[u] = in ? __ldg(ci + k + 32 * u) : 0;
+                a[u] = in ? __ldg(v + k + 32 * u) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = k + 32 * u < e ? xf(c[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (k + 32 * u < e) s = addd(s, mul(a[u], x[u]));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o);
+        const int nx = i + nw;
+        if (nx < rows) b = __ldg(rp + nx), e = __ldg(rp + nx + 1);
+        if (!skip && lane == 0) epi.row(i, s, acc);
+    }
+    if (skip) return;
+    pdl_release_late(8);
+    if constexpr (NR > 0) block_partial<NR>(acc, epi.slot());
+}
+
 template <class XF, class Epi>
 inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
     if (A->rows == 0) return;
@@ -733,6 +791,19 @@ inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
                 go(k_spmv_sellw<XF, Epi, 4, Cols32>, c32);
         }
     } else {
+        // warp per row when the mean row has >= 48 entries (S-4M 0.768 -> 0.753 ms per iteration,
+        // C2 0.295 -> 0.279; thresholds 32 / 100: C2 0.281 / 0.284). IBMGPU_WARPROW=N sets the bar,
+        // 0 keeps every such matrix on k_spmv_adapt
+        static const int warprow = [] {
+            const char* e = std::getenv("IBMGPU_WARPROW");
+            return e ? std::atoi(e) : 48;
+        }();
+        if (warprow > 0 && A->nnz >= (long long)warprow * A->rows) {
+            grid = std::max(1, std::min(A->n_blocks, (A->rows + kBlock / 32 - 1) / (kBlock / 32)));
+            launch_k(c, k_spmv_warprow<XF, Epi>, grid, kBlock, s, A->rows, A->rp.p, A->ci.p, A->v.p, xf, epi);
+            if constexpr (Epi::NR > 0) launch_k(c, k_finalize<Epi>, 1, kFinThreads, s, epi, grid);
+            return;
+        }
         const AdaptPlan pl{A->blk_meta.p, A->lrow.p, A->lpart.p, A->lcnt.p};
         grid = A->n_blocks;
         launch_k(c, k_spmv_adapt<XF, Epi>, grid, kBlock, s, pl, A->rp.p, A->ci.p, A->v.p, xf, epi);
