@@ -353,6 +353,22 @@ def case_probe(args, name: str) -> dict:
 
 
 def flapping_probe(args) -> dict:
+    """The moving-body probe in its own process, as the reference's own runner would run the case.
+    In the bench process, after the S-4M and C2 runs, it still swings (30-104 steps/s on one build;
+    fresh processes 100-104), with the operator pipeline's waits growing; see DESIGN.md (d)."""
+    import subprocess
+    code = ("import json, sys; sys.path.insert(0, %r); import bench; "
+            "print(json.dumps(bench.flapping_probe_inproc(None)))" % ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    if r.returncode != 0 or not lines:
+        raise RuntimeError("flapping probe failed: " + r.stderr[-500:])
+    out = json.loads(lines[-1])
+    out["process"] = "separate"
+    return out
+
+
+def flapping_probe_inproc(args) -> dict:
     """Moving body (BASELINE configs[3]): E, H, Q, Q^T, lhs2 rebuilt every step and the SA hierarchy
     every n_pc steps, all on the device. Wall clock around whole Stepper.advance calls."""
     from paper_1109_3524_b200 import ibm
