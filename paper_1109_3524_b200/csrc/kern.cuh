@@ -685,29 +685,33 @@ __global__ void __launch_bounds__(kBlock, IBMGPU_ADAPT_MINB) k_spmv_adapt(AdaptP
 // the mean row has >= 48 entries): lanes stride the row four entries at a time with every load of
 // a batch issued first (the last, partial batch too), then five shuffle steps. Deterministic (fixed order), not bitwise with spmv_into — the
 // same contract as the adaptive kernel. Warps take rows gw, gw + warps, ...
-template <class XF, class Epi>
+template <class XF, class Epi, int TPR = 32>
 __global__ void __launch_bounds__(kBlock, 8) k_spmv_warprow(int rows, const int* __restrict__ rp,
                                                              const int* __restrict__ ci, const double* __restrict__ v,
                                                              XF xf, Epi epi) {
     pdl_release_early(8);
     constexpr int NR = Epi::NR;
+    constexpr int G = 32 / TPR;  // rows per warp pass
     double acc[NR > 0 ? NR : 1];
 #pragma unroll
     for (int r = 0; r < (NR > 0 ? NR : 1); ++r) acc[r] = 0.0;
-    const int lane = threadIdx.x & 31;
-    const int nw = gridDim.x * (kBlock / 32);
-    int i = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & (TPR - 1), gi = (threadIdx.x & 31) / TPR;
+    const int nwr = gridDim.x * (kBlock / 32) * G;  // rows per grid pass
+    // warp-uniform pass base: every lane runs every pass (the shuffles need the whole warp)
+    int r0 = (blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5)) * G;
+    int i = r0 + gi;
     int b = i < rows ? __ldg(rp + i) : 0, e = i < rows ? __ldg(rp + i + 1) : 0;
     pdl_wait();
     const bool skip = epi.skip();
-    for (; i < rows; i += nw) {
+    for (; r0 < rows; r0 += nwr) {
+        i = r0 + gi;
         double s = 0.0;
         int k = b + lane;
-        for (; k + 96 < e; k += 128) {
+        for (; k + 3 * TPR < e; k += 4 * TPR) {
             int c[4];
             double a[4], x[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) c[u] = __ldg(ci + k + 32 * u), a[u] = __ldg(v + k + 32 * u);
+            for (int u = 0; u < 4; ++u) c[u] = __ldg(ci + k + TPR * u), a[u] = __ldg(v + k + TPR * u);
 #pragma unroll
             for (int u = 0; u < 4; ++u) x[u] = xf(c[u]);
 #pragma unroll
@@ -718,21 +722,22 @@ __global__ void __launch_bounds__(kBlock, 8) k_spmv_warprow(int rows, const int*
             double a[4], x[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const bool in = k + 32 * u < e;
-                c[u] = in ? __ldg(ci + k + 32 * u) : 0;
-                a[u] = in ? __ldg(v + k + 32 * u) : 0.0;
+                const bool in = k + TPR * u < e;
+                c[u] = in ? __ldg(ci + k + TPR * u) : 0;
+                a[u] = in ? __ldg(v + k + TPR * u) : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) x[u] = k + 32 * u < e ? xf(c[u]) : 0.0;
+            for (int u = 0; u < 4; ++u) x[u] = k + TPR * u < e ? xf(c[u]) : 0.0;
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (k + 32 * u < e) s = addd(s, mul(a[u], x[u]));
+                if (k + TPR * u < e) s = addd(s, mul(a[u], x[u]));
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o);
-        const int nx = i + nw;
+        for (int o = TPR / 2; o > 0; o >>= 1) s += __shfl_down_sync(kFull, s, o, TPR);
+        const int nx = i + nwr;
+        b = e = 0;
         if (nx < rows) b = __ldg(rp + nx), e = __ldg(rp + nx + 1);
-        if (!skip && lane == 0) epi.row(i, s, acc);
+        if (!skip && lane == 0 && i < rows) epi.row(i, s, acc);
     }
     if (skip) return;
     pdl_release_late(8);
@@ -798,9 +803,19 @@ inline void launch_spmv(Ctx* c, const Mat* A, XF xf, Epi epi, cudaStream_t s) {
             const char* e = std::getenv("IBMGPU_WARPROW");
             return e ? std::atoi(e) : 48;
         }();
+        static const int warprow16 = [] {  // IBMGPU_WARPROW16=N: half-warp rows for means in [N, 48) (A/B)
+            const char* e = std::getenv("IBMGPU_WARPROW16");
+            return e ? std::atoi(e) : 0;
+        }();
         if (warprow > 0 && A->nnz >= (long long)warprow * A->rows) {
             grid = std::max(1, std::min(A->n_blocks, (A->rows + kBlock / 32 - 1) / (kBlock / 32)));
-            launch_k(c, k_spmv_warprow<XF, Epi>, grid, kBlock, s, A->rows, A->rp.p, A->ci.p, A->v.p, xf, epi);
+            launch_k(c, k_spmv_warprow<XF, Epi, 32>, grid, kBlock, s, A->rows, A->rp.p, A->ci.p, A->v.p, xf, epi);
+            if constexpr (Epi::NR > 0) launch_k(c, k_finalize<Epi>, 1, kFinThreads, s, epi, grid);
+            return;
+        }
+        if (warprow16 > 0 && A->nnz >= (long long)warprow16 * A->rows) {
+            grid = std::max(1, std::min(A->n_blocks, (A->rows + kBlock / 16 - 1) / (kBlock / 16)));
+            launch_k(c, k_spmv_warprow<XF, Epi, 16>, grid, kBlock, s, A->rows, A->rp.p, A->ci.p, A->v.p, xf, epi);
             if constexpr (Epi::NR > 0) launch_k(c, k_finalize<Epi>, 1, kFinThreads, s, epi, grid);
             return;
         }
